@@ -1,0 +1,114 @@
+/*
+ * girg_oracle.h -- the CPU ORACLE for the GIRG hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load or call this library.  The product
+ * path (paper_1905_06706_b200/, include/girg.h) never links, imports or executes it,
+ * and this oracle shares no code, header, table or constant generator with it.
+ *
+ * Plain, sequential, obviously-correct C99 (compiled -O2 -ffp-contract=off, glibc libm).
+ * Citations: "P:NNN" = line NNN of /root/reference/PAPER.md (arXiv:1905.06706).
+ * Every reading of an ambiguous passage is listed in DESIGN.md ("Readings", R1..R20).
+ *
+ * Parity status of every function is pinned by tests/test_oracle_*.py; see DESIGN.md
+ * section "Oracle pins".  No function here is "parity unpinned".
+ */
+#ifndef GIRG_ORACLE_H
+#define GIRG_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (same numeric meaning as the C ABI, defined independently) */
+#define OR_OK 0
+#define OR_EINVAL (-1)
+#define OR_ECAPACITY (-2)
+#define OR_ERANGE (-3)
+#define OR_ENOMEM (-4)
+
+/* ---- randomness (R17: counter-based, keyed; replaces P:1281 thread-local RNG) ---- */
+void or_philox4x32_10(const uint32_t ctr[4], uint64_t seed, uint32_t out[4]);
+double or_u53(uint32_t hi, uint32_t lo);
+
+/* ---- model, Sec. 2.1 P:258-290 ---- */
+int or_weights(uint64_t n, double beta, uint64_t seed, double *w);          /* P:264-265, R4 */
+double or_weight_of_uniform(double U, double beta); /* inverse transform (1-U)^(-1/(beta-1)) */
+int or_positions(uint64_t n, int d, uint64_t seed, double *x /* [d][n] */);
+double or_exact_sum(const double *w, uint64_t n);                         /* P:265-266, R3 */
+double or_torus_dist(const double *xu, const double *xv, int d);
+double or_dpow(double dist, int d);                                       /* ||.||^d, left to right */
+/* scaled weight product q = (w_u*w_v)*s, s = kappa/W  (R1) */
+double or_prob(double wu, double wv, double s, double D, double T);       /* Eq. 1, R1 */
+int or_thresh_edge(double wu, double wv, double s, double D);             /* P:282-286, R1 */
+
+/* ---- Morton / grid, Sec. 4.4, Sec. 5.2 P:663-669 ---- */
+uint32_t or_morton_encode(const uint32_t *coord, int d, int level);
+void or_morton_decode(uint32_t code, int d, int level, uint32_t *coord);
+uint32_t or_cell_of_point(const double *x, int d, int level); /* x: d contiguous coords */
+int or_are_neighbors(uint32_t A, uint32_t B, int d, int level); /* Fig. 2a, R8 */
+int or_delta_max(uint32_t A, uint32_t B, int d, int level);     /* max_k torus cell gap */
+
+/* ---- levels, Sec. 4.1 P:440-476 ---- */
+typedef struct {
+    int L;           /* number of layers = e_max - e_min + 1 */
+    int e_min;       /* min ilogb(w) */
+    int Lmax;        /* depth cap, R7 */
+    int maxCL;       /* max CL over nonempty layer pairs */
+    double W, s;     /* exact sum, s = kappa/W */
+    uint64_t cnt[64];
+    int CL[64][64];
+    int I[64];
+} or_levels_t;
+int or_levels(const double *w, uint64_t n, int d, double kappa, or_levels_t *lv);
+
+/* ---- work counters and near-tie log (north-star parity rule) ---- */
+typedef struct {
+    uint64_t visits;          /* cell pairs visited by the recursion */
+    uint64_t ev1, ev1_nonempty, cand1, acc1; /* type-I events, nonempty, candidates, edges */
+    uint64_t ev2, ev2_nonempty, chunks, draws, landings, acc2; /* type-II */
+    uint64_t nt1, nt2acc, nt2jump; /* near-ties: type-I r~p, type-II r_acc~p/pbar, jump z~int */
+    uint64_t cand2;                /* sum of |V_i^A||V_j^B| over type-II events */
+} or_stats_t;
+
+/* Edge sampler: Algorithm 1 over the Lemma-1 index, double counting
+ * per App. B.1 (R16), type-II by geometric jumps (R10).
+ * Shard filter: only events whose A cell's block at shard_level lies in
+ * [blk_lo, blk_hi) are processed; shard_level=0, [0,1) = everything.
+ * edges: [cap][2] uint32 (u<v).  Returns OR_OK / OR_ECAPACITY (m_out = true m) / errors. */
+int or_edges(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
+             uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi,
+             uint32_t *edges, uint64_t cap, uint64_t *m_out, or_stats_t *st);
+
+/* test hooks: instrumented coverage (cover: n*n counters), Lemma-1 index export, and the
+ * per-level cell-pair counts of Algorithm 1 on a full tree */
+int or_coverage(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
+                uint32_t *cover, or_stats_t *st);
+int or_index(const double *w, const double *x, uint64_t n, int d, double kappa, uint32_t *order,
+             uint64_t *lstart, uint32_t *P, uint64_t *poff, uint64_t pcap);
+int or_count_pairs(int d, int depth, uint64_t *nb, uint64_t *ds, uint64_t *ds2, uint64_t *ds3);
+
+/* O(n^2) brute force, threshold model (T=0), canonical arithmetic */
+int or_bruteforce_t0(const double *w, const double *x, uint64_t n, int d, double kappa,
+                     uint32_t *edges, uint64_t cap, uint64_t *m_out);
+/* O(n^2) sum_{u<v} p_uv  (expected edge count given w, x) */
+double or_expected_edges_bf(const double *w, const double *x, uint64_t n, int d, double T,
+                            double kappa);
+
+/* ---- average-degree estimation, Sec. 5.1, App. B.2 P:1059-1158 ---- */
+double or_g(double y, double T);                 /* E[X_uv] given y = 2^d kappa w_u w_v / W */
+double or_f_bruteforce(const double *w, uint64_t n, int d, double T, double kappa);
+double or_f(const double *w, uint64_t n, int d, double T, double kappa); /* O(n + |R|) */
+double or_ER_quadratic(const double *w, uint64_t n, int d, double T, double kappa);
+double or_ER_linear(const double *w, uint64_t n, int d, double T, double kappa);
+int or_scale_weights(const double *w, uint64_t n, double avg_deg, int d, double T,
+                     double beta, double *kappa_out);
+
+/* single geometric skip, P:494-501 (R10): floor(log(1-u)/log1p(-p)) */
+int64_t or_geometric_skip(double p, double u);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

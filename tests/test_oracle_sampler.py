@@ -1,0 +1,176 @@
+"""Pins for the oracle's edge sampler (Algorithm 1, type-I/type-II) -- CPU only.
+
+T = 0: the method computes exactly the plain threshold graph, so the oracle must equal the O(n^2)
+brute force bit for bit.  T > 0: the result is random; the oracle is pinned by per-pair
+frequencies against Eq. 1, expected edge counts against sum_{u<v} p_uv, exact coverage of the
+candidate pairs by events, the T -> 0 limit and structural invariants.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from workloads import synth_inputs
+
+
+def keys(e):
+    return np.sort((e[:, 0].astype(np.uint64) << np.uint64(32)) | e[:, 1].astype(np.uint64))
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("beta", [2.2, 2.5, 2.8, 3.0])
+def test_threshold_equals_bruteforce(oracle, d, beta):
+    """T=0 sampler == O(n^2) brute force for n in {200,1000,2000}, several seeds."""
+    for n, seed in ((200, 1), (1000, 2), (2000, 3), (2000, 4)):
+        w, x = synth_inputs(n, d, beta, 1000 * d + seed)
+        kappa = oracle.scale_weights(w, 10.0, d, 0.0, beta)
+        e = oracle.edges(w, x, d, 0.0, kappa, seed)
+        b = oracle.bruteforce_t0(w, x, d, kappa)
+        assert np.array_equal(keys(e), keys(b)), (n, seed)
+
+
+def test_threshold_C1_full_bruteforce(oracle):
+    """BASELINE config 1 itself (n = 10^4, d = 1, beta = 2.8, T = 0), all 5*10^7 pairs."""
+    w, x = synth_inputs(10_000, 1, 2.8, 1)
+    kappa = oracle.scale_weights(w, 10.0, 1, 0.0, 2.8)
+    e, st = oracle.edges(w, x, 1, 0.0, kappa, 1, with_stats=True)
+    b = oracle.bruteforce_t0(w, x, 1, kappa)
+    assert np.array_equal(keys(e), keys(b))
+    assert abs(2 * len(e) / 10_000 - 10.0) < 0.6
+    assert st["ev2"] == 0  # no type-II events at T = 0
+
+
+@pytest.mark.parametrize("d,T", [(1, 0.5), (2, 0.8), (3, 0.9), (1, 0.2)])
+def test_coverage_each_pair_exactly_once(oracle, d, T):
+    """every unordered vertex pair is a candidate of exactly one (cell pair, bucket pair)
+    event -- instrumented oracle on n <= 600."""
+    n = 600 if d < 3 else 400
+    w, x = synth_inputs(n, d, 2.3, 77 + d)
+    kappa = oracle.scale_weights(w, 4.0, d, T, 2.3)
+    cov, st = oracle.coverage(w, x, d, T, kappa)
+    sym = cov.astype(np.int64) + cov.T.astype(np.int64)
+    assert (np.diag(cov) == 0).all()
+    off = ~np.eye(n, dtype=bool)
+    assert (sym[off] == 1).all()
+    assert st["ev2_nonempty"] > 0 and st["ev1_nonempty"] > 0
+    assert st["cand1"] + st["cand2"] == n * (n - 1) // 2
+
+
+@pytest.mark.parametrize("d,T,runs", [(1, 0.5, 20000), (2, 0.8, 20000), (1, 0.3, 8000), (3, 0.9, 8000)])
+def test_per_pair_frequency(oracle, d, T, runs):
+    """with fixed w and x, each pair's empirical edge frequency over independent edge
+    seeds is within 5 sigma of p_uv (Eq. 1), and the chi-square over pairs is plausible."""
+    n = 40
+    w, x = synth_inputs(n, d, 2.5, 5 + d)
+    kappa = oracle.scale_weights(w, 3.0, d, T, 2.5)
+    W = oracle.exact_sum(w)
+    s = kappa / W
+    P = np.zeros((n, n))
+    for u in range(n):
+        for v in range(u + 1, n):
+            D = oracle.dpow(oracle.torus_dist(x[:, u], x[:, v]), d)
+            P[u, v] = oracle.prob(w[u], w[v], s, D, T)
+    cnt = np.zeros((n, n))
+    land = 0
+    for seed in range(runs):
+        e, st = oracle.edges(w, x, d, T, kappa, seed + 1, with_stats=True)
+        land += st["landings"]
+        cnt[e[:, 0], e[:, 1]] += 1
+    assert land > 0  # type-II jumps were exercised
+    iu = np.triu_indices(n, 1)
+    p, f = P[iu], cnt[iu] / runs
+    sure = p >= 1.0
+    assert (f[sure] == 1.0).all()
+    q = p[~sure]
+    c = cnt[iu][~sure]
+    assert (c[q == 0] == 0).all()
+    # exact two-sided binomial p-value per pair, Bonferroni over pairs (normal z is wrong for
+    # pairs with expected counts << 1)
+    from scipy import stats
+    pv = np.minimum(1.0, 2 * np.minimum(stats.binom.cdf(c, runs, q), stats.binom.sf(c - 1, runs, q)))
+    assert pv[q > 0].min() * (q > 0).sum() > 1e-4, pv[q > 0].min()
+    sig = np.sqrt(q * (1 - q) / runs)
+    z = np.abs(f[~sure] - q) / np.maximum(sig, 1e-300)
+    live = (q > 1e-3) & (q < 1 - 1e-3)
+    chi2 = float(np.sum(z[live] ** 2))
+    k = int(live.sum())
+    assert abs(chi2 - k) < 6 * math.sqrt(2 * k), (chi2, k)
+
+
+def test_expected_edge_count(oracle):
+    """mean of m over independent edge seeds vs sum_{u<v} p_uv (brute force), z < 4."""
+    n, d, T = 3000, 2, 0.5
+    w, x = synth_inputs(n, d, 2.5, 9)
+    kappa = oracle.scale_weights(w, 8.0, d, T, 2.5)
+    mu = oracle.expected_edges_bf(w, x, d, T, kappa)
+    ms = np.array([len(oracle.edges(w, x, d, T, kappa, s)) for s in range(1, 61)])
+    # var(m) = sum p(1-p) <= mu
+    z = abs(ms.mean() - mu) / math.sqrt(mu / len(ms))
+    assert z < 4, (ms.mean(), mu)
+
+
+def test_structure_and_determinism(oracle):
+    for d, T in ((1, 0.5), (2, 0.8), (3, 0.6)):
+        n = 5000
+        w, x = synth_inputs(n, d, 2.4, 31 + d)
+        kappa = oracle.scale_weights(w, 10.0, d, T, 2.4)
+        e = oracle.edges(w, x, d, T, kappa, 7)
+        assert (e[:, 0] < e[:, 1]).all() and (e[:, 1] < n).all()
+        k = keys(e)
+        assert len(np.unique(k)) == len(k)
+        assert np.array_equal(k, keys(oracle.edges(w, x, d, T, kappa, 7)))
+        assert not np.array_equal(k, keys(oracle.edges(w, x, d, T, kappa, 8)))
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_shards_partition_the_edge_set(oracle, d):
+    """events are owned by the block of their A cell; shards are disjoint and
+    their union is the full edge set (also exercised by the gloo multi-process test)."""
+    n, T = 4000, 0.7
+    w, x = synth_inputs(n, d, 2.3, 51 + d)
+    kappa = oracle.scale_weights(w, 10.0, d, T, 2.3)
+    full = keys(oracle.edges(w, x, d, T, kappa, 3))
+    for sl in (1, 2, 3):
+        nb = 1 << (d * sl)
+        cuts = sorted(set([0, nb // 3, nb // 2, nb]))
+        parts = [keys(oracle.edges(w, x, d, T, kappa, 3, shard=(sl, a, b))) for a, b in zip(cuts, cuts[1:])]
+        allp = np.concatenate(parts)
+        assert len(allp) == len(full)
+        assert np.array_equal(np.sort(allp), full)
+
+
+def test_capacity_error_and_rerun(oracle):
+    """ECAPACITY reports the true m; re-running with enough capacity gives the same set."""
+    import ctypes as C
+
+    n, d, T = 3000, 1, 0.5
+    w, x = synth_inputs(n, d, 2.5, 3)
+    kappa = oracle.scale_weights(w, 10.0, d, T, 2.5)
+    full = oracle.edges(w, x, d, T, kappa, 5)
+    out = np.empty((10, 2), dtype=np.uint32)
+    m = C.c_uint64(0)
+    rc = oracle.lib().or_edges(oracle._dp(w), oracle._dp(x), n, d, T, kappa, 5, 0, 0, 1,
+                               oracle._u32p(out), 10, C.byref(m), None)
+    assert rc == oracle.ECAPACITY and int(m.value) == len(full)
+    assert np.array_equal(keys(oracle.edges(w, x, d, T, kappa, 5, cap=len(full))), keys(full))
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_T_to_zero_limit(oracle, d):
+    """P:319-320 / P:107-108: as T -> 0 the binomial model becomes the threshold model.  For
+    fixed kappa the symmetric difference E_T ^ E_0 consists of the long pairs (D > q) that
+    happen to be T-edges: expected sum_{D>q} (q/D)^(1/T) = sum_{u<v} p_uv - |E_0|, -> 0."""
+    n = 1500
+    w, x = synth_inputs(n, d, 2.5, 61 + d)
+    kappa = oracle.scale_weights(w, 10.0, d, 0.0, 2.5)
+    E0 = set(keys(oracle.edges(w, x, d, 0.0, kappa, 1)).tolist())
+    sizes = []
+    for T in (1e-2, 1e-3, 1e-4):
+        mu = oracle.expected_edges_bf(w, x, d, T, kappa) - len(E0)
+        ET = set(keys(oracle.edges(w, x, d, T, kappa, 2)).tolist())
+        assert E0 <= ET  # every short pair has p = 1
+        diff = len(ET ^ E0)
+        assert abs(diff - mu) <= 5 * math.sqrt(mu) + 1, (T, diff, mu)
+        sizes.append(diff)
+    assert sizes[0] >= sizes[-1]
+    assert sizes[-1] <= 3
