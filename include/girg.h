@@ -1,0 +1,159 @@
+/*
+ * girg.h -- C ABI of the B200-native GIRG edge generator (libgirg.so).
+ *
+ * The operations follow the problem statement of arXiv:1905.06706 ("Efficiently generating
+ * geometric inhomogeneous and hyperbolic random graphs"); "P:NNN" cites a line of its text
+ * (PAPER.md).  All arithmetic runs in the library's sm_100a kernels; the host side only
+ * validates arguments, computes O(#layers^2) tables and launches kernels.
+ *
+ * Conventions shared by every entry point
+ *   - Pointers named *_dev are caller-owned DEVICE buffers (e.g. torch CUDA tensors); pointers
+ *     named *_host / *_out are caller-owned HOST memory.  The library never frees or retains a
+ *     caller pointer after the call returns.
+ *   - Scratch memory is allocated stream-ordered (cudaMallocAsync on the current device's
+ *     default pool) and released before return.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All work is enqueued on it.
+ *     Calls on different streams may run concurrently from different host threads.
+ *   - Return value: GIRG_OK (0) or a negative girg_status.  Arguments are validated before any
+ *     launch; no C++ exception crosses the ABI.
+ *   - Layout of positions: structure of arrays, x[k*n + v] = coordinate k of vertex v, k < d.
+ *   - Vertex ids are uint32, so n < 2^32.
+ */
+#ifndef GIRG_H
+#define GIRG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GIRG_OK = 0,
+    GIRG_EINVAL = -1,    /* invalid argument (value, pointer, non-finite input) */
+    GIRG_ECAPACITY = -2, /* edge buffer too small; *m_out holds the true edge count */
+    GIRG_ERANGE = -3,    /* input outside the representable range of the index (see below) */
+    GIRG_ENOMEM = -4,    /* device allocation failed */
+    GIRG_ECUDA = -5      /* a CUDA runtime error; see girg_strerror / girg_last_cuda_error */
+} girg_status;
+
+/* Optional work counters of one girg_edges call (pass NULL to skip collecting them). */
+typedef struct {
+    uint64_t cand1;      /* type-I candidate pairs tested */
+    uint64_t ev2;        /* nonempty type-II events */
+    uint64_t chunks;     /* type-II jump chains                                  */
+    uint64_t draws;      /* type-II Philox draws                                 */
+    uint64_t landings;   /* type-II candidates reached by a jump                 */
+    uint64_t edges1;     /* edges from type-I events                             */
+    uint64_t edges2;     /* edges from type-II events                            */
+    uint64_t neartie1;   /* |r - p_uv| < 1e-12 at a type-I test (device-side)    */
+    uint64_t neartie2;   /* |r_acc - p_uv/pbar| < 1e-12 at a type-II acceptance  */
+    uint64_t layers;     /* number of weight layers (buckets)                    */
+    uint64_t key_space;  /* number of index cells sum_i 2^(d I(i))               */
+} girg_stats;
+
+/*
+ * girg_weights -- power-law weights, P:264-265 ("weights w_1..w_n following a power law with
+ * exponent beta > 2").  Pareto law with w_min = 1, P(w >= x) = x^(1-beta), by inverse transform
+ * w_v = (1-U_v)^(-1/(beta-1)); U_v is the 53-bit uniform from Philox4x32-10 counter (v,0,0,1),
+ * key = seed.  Output w_dev[n] (float64).  Asynchronous.
+ * Errors: EINVAL if n == 0, n >= 2^32, beta <= 2 or non-finite, w_dev == NULL.
+ */
+int girg_weights(uint64_t n, double beta, uint64_t seed, double *w_dev, void *stream);
+
+/*
+ * girg_positions -- uniform positions on the torus T^d = [0,1)^d.  Coordinates 2k
+ * and 2k+1 of vertex v are the two 53-bit uniforms of Philox4x32-10 counter (v,k,0,2).
+ * Output x_dev[d*n] (SoA, float64, on the 2^-53 grid).  Asynchronous.
+ * Errors: EINVAL if n == 0, n >= 2^32, d not in [1,5], x_dev == NULL.
+ */
+int girg_positions(uint64_t n, int d, uint64_t seed, double *x_dev, void *stream);
+
+/*
+ * girg_scale_weights -- average-degree estimation, Sec. 5.1 P:627-658 and App. B.2
+ * finds kappa such that the expected average degree f(kappa) of the GIRG with
+ * weights w_dev[n], dimension d and temperature T equals avg_deg (exponential search and
+ * bisection on the monotone f; f evaluated exactly from the actual weights, with the
+ * saturated pairs E_R handled in O(|R|)).  kappa is the constant of the kappa form used by
+ * girg_edges: p_uv = min(1, (kappa w_u w_v / (W ||x_u-x_v||^d))^(1/T)), i.e. kappa = c^T for
+ * Eq. 1 (App. B.2 P:1073-1075 "scaling all weights by c^T"), kappa = c^d for T = 0.
+ * beta only seeds the search (kappa0 = avg_deg (1-T) / (2^d (beta-1)/(beta-2))).
+ * Writes *kappa_out (host).  Synchronises `stream`.
+ * Errors: EINVAL if n < 2, avg_deg not in (0, n-1), d not in [1,5], T not in [0,1),
+ * beta <= 2, a weight not finite and > 0; ERANGE if f overflows (extreme T / weights).
+ */
+int girg_scale_weights(const double *w_dev, uint64_t n, double avg_deg, int d, double T,
+                       double beta, double *kappa_out, void *stream);
+
+/*
+ * girg_edges -- sample the GIRG edge set in expected linear time: weight layers,
+ * the nested Morton-ordered grid and Lemma-1 index, and per layer pair the
+ * neighbouring (type-I) cell pairs tested pair by pair and the distant (type-II) cell pairs
+ * sampled by geometric jumps under the cell-pair bound pbar with rejection (Sec. 4.2-4.3,
+ * Algorithm 1).
+ *   T = 0 : threshold model, edge iff ||x_u-x_v||^d <= kappa w_u w_v / W.
+ *   T > 0 : binomial model, independent edges with p_uv = min(1,(kappa w_u w_v/(W D))^(1/T)).
+ * Inputs: w_dev[n] (finite, > 0), x_dev[d*n] (each coordinate in [0,1)), 0 <= T < 1,
+ * kappa > 0 finite, seed (keys all Philox draws; the edge set is a pure function of
+ * (w, x, d, T, kappa, seed) and does not depend on the schedule).
+ * Output: edges_dev[cap][2] uint32 pairs (u, v) with u < v, in unspecified order, no
+ * duplicates, no self-loops; *m_out (host) = number of edges.  Synchronises `stream`.
+ * Errors: EINVAL (bad argument / input value), ECAPACITY (m > cap: *m_out = true m, buffer
+ * contents unspecified; re-running with cap >= m gives the identical set), ERANGE (more than
+ * 64 weight layers, weights outside [2^-500, 2^500], d*I(i) > 31 or index cells >= 2^32-1),
+ * ENOMEM, ECUDA.
+ */
+int girg_edges(const double *w_dev, const double *x_dev, uint64_t n, int d, double T,
+               double kappa, uint64_t seed, uint32_t *edges_dev, uint64_t cap,
+               uint64_t *m_out, void *stream);
+
+/*
+ * girg_edges_shard -- girg_edges restricted to the events whose A cell (the cell of the
+ * lower layer) lies in Morton blocks [blk_lo, blk_hi) at level shard_level (coarser events are
+ * owned by the block of their first descendant).  Shards of one graph are disjoint and their
+ * union is the girg_edges result (multi-GPU partitioning).
+ * shard_level = 0, blk_lo = 0, blk_hi = 1 is the whole graph.  stats_out may be NULL.
+ * Errors: as girg_edges, plus EINVAL if shard_level*d > 32 or blk_lo >= blk_hi.
+ */
+int girg_edges_shard(const double *w_dev, const double *x_dev, uint64_t n, int d, double T,
+                     double kappa, uint64_t seed, int shard_level, uint64_t blk_lo,
+                     uint64_t blk_hi, uint32_t *edges_dev, uint64_t cap, uint64_t *m_out,
+                     girg_stats *stats_out, void *stream);
+
+/*
+ * girg_edges_host -- end-to-end variant with HOST buffers: copies w_host[n] and x_host[d*n]
+ * to the device, runs girg_edges and copies the edges back into edges_host[cap][2].
+ * Pinned (page-locked) host memory gives full copy bandwidth.  Same semantics and errors.
+ */
+int girg_edges_host(const double *w_host, const double *x_host, uint64_t n, int d, double T,
+                    double kappa, uint64_t seed, uint32_t *edges_host, uint64_t cap,
+                    uint64_t *m_out, void *stream);
+
+/* Phase timings of the last successful girg_edges / girg_edges_shard / girg_edges_host call on
+ * the calling host thread, measured with CUDA events recorded on the call's stream around each
+ * phase (the events cost ~1 us; they are always recorded). */
+typedef struct {
+    double ms_total;   /* whole call: first launch .. edge count read back (device clock)       */
+    double ms_wstats;  /* K0 weight statistics + host plan (includes the one mid-call sync)      */
+    double ms_index;   /* K1-K4 keys, scan, scatter, in-cell order / gather (Lemma-1 index)      */
+    double ms_sample;  /* K5 sampling kernel (type-I tests, type-II jumps, edge output)          */
+    uint64_t launches; /* kernels launched by the call                                          */
+    uint64_t n, m, key_space;
+    int d;
+    int pad;
+} girg_timings;
+int girg_last_timings(girg_timings *out);
+
+/* Human-readable text of a status code (static storage). */
+const char *girg_strerror(int status);
+
+/* The CUDA runtime error string of the last GIRG_ECUDA on this host thread ("" if none). */
+const char *girg_last_cuda_error(void);
+
+/* Library ABI version (major*100 + minor). */
+int girg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GIRG_H */

@@ -39,7 +39,7 @@ class Stats(C.Structure):
     _fields_ = [(name, C.c_uint64) for name in (
         "visits", "ev1", "ev1_nonempty", "cand1", "acc1",
         "ev2", "ev2_nonempty", "chunks", "draws", "landings", "acc2",
-        "nt1", "nt2acc", "nt2jump", "cand2")]
+        "nt1", "nt2acc", "nt2jump", "cand2", "ns_pre", "ns_edges")]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}

@@ -15,6 +15,7 @@
 
 #include <limits.h>
 #include <math.h>
+#include <time.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -412,7 +413,7 @@ static void type1(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
  * R10) are visited by geometric jumps with the cell-pair bound pbar and accepted with
  * probability p_uv/pbar (R14: r_acc*pbar < p_uv).  Chunking (R10): the candidate index range
  * is cut into chunks of C = 2^clog2 candidates, each an independent jump chain (exact by
- * memorylessness).  Draw k of chunk ch uses Philox counter
+ * memorylessness), at most 2^15 chunks per event.  Draw k of chunk ch uses Philox counter
  * (A, B, l | i<<5 | j<<11 | ch<<17, k): r_jump = (o0,o1), r_acc = (o2,o3). */
 static void type2(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
 {
@@ -435,9 +436,12 @@ static void type2(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
     size_t ti = TAB(c, i, j, l, cls);
     double pbar = c->pbar[ti], Lbar = c->Lbar[ti];
     if (pbar == 0.0) return;
-    uint64_t C = 1ull << c->clog2[ti];
+    /* R10: chunk length C = 2^clog2 (2..4 expected landings per chunk), doubled until the
+     * event has at most 2^15 chunks (the chunk index has 15 counter bits) */
+    int cl2 = c->clog2[ti];
+    while (((N - 1) >> cl2) >= (1ull << 15)) cl2++;
+    uint64_t C = 1ull << cl2;
     uint64_t nch = (N - 1) / C + 1;
-    if (nch > (1u << 15)) { c->err = OR_ERANGE; return; }
     const uint32_t *Va = c->order + c->lstart[i], *Vb = c->order + c->lstart[j];
     double xu[5], xv[5];
     for (uint64_t ch = 0; ch < nch; ch++) {
@@ -532,6 +536,13 @@ typedef struct {
     uint64_t pcap;
 } or_index_out;
 
+static uint64_t now_ns(void)
+{
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (uint64_t)ts.tv_sec * 1000000000ull + (uint64_t)ts.tv_nsec;
+}
+
 static int or_run(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
                   uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi,
                   uint32_t *edges, uint64_t cap, uint64_t *m_out, or_stats_t *st,
@@ -548,6 +559,7 @@ static int or_run(const double *w, const double *x, uint64_t n, int d, double T,
     for (uint64_t i = 0; i < (uint64_t)d * n; i++)
         if (!(x[i] >= 0.0 && x[i] < 1.0)) return OR_EINVAL;
 
+    uint64_t t0 = now_ns();
     or_ctx *c = (or_ctx *)calloc(1, sizeof(or_ctx));
     if (!c) return OR_ENOMEM;
     int rc = or_levels(w, n, d, kappa, &c->lv);
@@ -660,7 +672,10 @@ static int or_run(const double *w, const double *x, uint64_t n, int d, double T,
         rc = OR_OK;
         goto done;
     }
+    uint64_t t1 = now_ns();
     recur(c, 0, 0u, 0u);
+    st->ns_pre = t1 - t0;
+    st->ns_edges = now_ns() - t1;
     rc = c->err;
     *m_out = c->m;
     if (!rc && c->m > cap) rc = OR_ECAPACITY;

@@ -70,6 +70,7 @@ typedef struct {
     uint64_t ev2, ev2_nonempty, chunks, draws, landings, acc2; /* type-II */
     uint64_t nt1, nt2acc, nt2jump; /* near-ties: type-I r~p, type-II r_acc~p/pbar, jump z~int */
     uint64_t cand2;                /* sum of |V_i^A||V_j^B| over type-II events */
+    uint64_t ns_pre, ns_edges;     /* wall time: levels + index ("Pre"), recursion ("Edges") */
 } or_stats_t;
 
 /* Edge sampler: Algorithm 1 over the Lemma-1 index, double counting

@@ -1,0 +1,179 @@
+"""paper_1905_06706_b200 -- B200-native (sm_100a) GIRG edge generator (arXiv:1905.06706).
+
+Thin ctypes binding over the C ABI in ``include/girg.h`` (``libgirg.so``, built in-tree).
+The functions below only marshal arguments: every step of the path runs in the library's
+CUDA kernels.  PyTorch provides device memory and the current CUDA stream.  There is no CPU
+fallback: if ``libgirg.so`` cannot be loaded, the import fails loudly.
+
+    w = girg.weights(n, beta, seed)                    # torch.float64 [n] on cuda
+    x = girg.positions(n, d, seed)                     # torch.float64 [d, n] on cuda
+    kappa = girg.scale_weights(w, avg_deg, d, T, beta) # float
+    e = girg.edges(w, x, T, kappa, seed)               # torch.int32 view of uint32 [m, 2], u < v
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from ._build import LIB as _LIB_PATH
+
+OK, EINVAL, ECAPACITY, ERANGE, ENOMEM, ECUDA = 0, -1, -2, -3, -4, -5
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        f"libgirg.so not built ({_LIB_PATH}); run `python -c 'import __graft_entry__ as g; g.build()'`")
+
+_lib = C.CDLL(_LIB_PATH)
+
+
+class Stats(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in (
+        "cand1", "ev2", "chunks", "draws", "landings", "edges1", "edges2",
+        "neartie1", "neartie2", "layers", "key_space")]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
+class Timings(C.Structure):
+    _fields_ = [("ms_total", C.c_double), ("ms_wstats", C.c_double), ("ms_index", C.c_double),
+                ("ms_sample", C.c_double), ("launches", C.c_uint64), ("n", C.c_uint64), ("m", C.c_uint64),
+                ("key_space", C.c_uint64), ("d", C.c_int), ("pad", C.c_int)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad"}
+
+
+_u64, _d, _i, _vp = C.c_uint64, C.c_double, C.c_int, C.c_void_p
+_lib.girg_weights.argtypes = [_u64, _d, _u64, _vp, _vp]
+_lib.girg_positions.argtypes = [_u64, _i, _u64, _vp, _vp]
+_lib.girg_scale_weights.argtypes = [_vp, _u64, _d, _i, _d, _d, C.POINTER(_d), _vp]
+_lib.girg_edges.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, _vp, _u64, C.POINTER(_u64), _vp]
+_lib.girg_edges_shard.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, _i, _u64, _u64, _vp, _u64,
+                                  C.POINTER(_u64), C.POINTER(Stats), _vp]
+_lib.girg_edges_host.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, _vp, _u64, C.POINTER(_u64), _vp]
+_lib.girg_last_timings.argtypes = [C.POINTER(Timings)]
+_lib.girg_strerror.argtypes = [_i]
+_lib.girg_strerror.restype = C.c_char_p
+_lib.girg_last_cuda_error.restype = C.c_char_p
+for _f in ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
+           "girg_edges_host", "girg_version", "girg_last_timings"):
+    getattr(_lib, _f).restype = C.c_int
+
+EXPORTS = ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
+           "girg_edges_host", "girg_strerror", "girg_last_cuda_error", "girg_version", "girg_last_timings")
+
+
+class GirgError(RuntimeError):
+    def __init__(self, code: int):
+        msg = _lib.girg_strerror(code).decode()
+        if code == ECUDA:
+            msg += ": " + _lib.girg_last_cuda_error().decode()
+        super().__init__(f"girg status {code}: {msg}")
+        self.code = code
+
+
+def _check(rc: int):
+    if rc != OK:
+        raise GirgError(rc)
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dev_f64(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous float64 CUDA tensor")
+    return t
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def version() -> int:
+    return _lib.girg_version()
+
+
+def weights(n: int, beta: float, seed: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Power-law weights (include/girg.h girg_weights)."""
+    w = out if out is not None else torch.empty(n, dtype=torch.float64, device="cuda")
+    _dev_f64(w, "out")
+    _check(_lib.girg_weights(n, beta, seed, w.data_ptr(), _stream(stream)))
+    return w
+
+
+def positions(n: int, d: int, seed: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Uniform torus positions, SoA [d, n] (include/girg.h girg_positions)."""
+    x = out if out is not None else torch.empty((d, n), dtype=torch.float64, device="cuda")
+    _dev_f64(x, "out")
+    _check(_lib.girg_positions(n, d, seed, x.data_ptr(), _stream(stream)))
+    return x
+
+
+def scale_weights(w: torch.Tensor, avg_deg: float, d: int, T: float, beta: float, stream=None) -> float:
+    """kappa for a target expected average degree (include/girg.h girg_scale_weights)."""
+    _dev_f64(w, "w")
+    k = C.c_double(0.0)
+    _check(_lib.girg_scale_weights(w.data_ptr(), w.numel(), avg_deg, d, T, beta, C.byref(k), _stream(stream)))
+    return k.value
+
+
+def edges(w: torch.Tensor, x: torch.Tensor, T: float, kappa: float, seed: int, cap: int | None = None,
+          out: torch.Tensor | None = None, shard=(0, 0, 1), stats: bool = False, stream=None):
+    """Sample the edge list (include/girg.h girg_edges / girg_edges_shard).
+
+    Returns an int32 CUDA tensor [m, 2] holding the uint32 pairs (u < v) (and the work counters
+    when ``stats``).  If ``cap`` (or ``out``) is too small the call is re-issued once with the
+    exact capacity the library reports."""
+    _dev_f64(w, "w")
+    _dev_f64(x, "x")
+    n = w.numel()
+    d = x.numel() // n
+    if x.numel() != d * n:
+        raise ValueError("x must have d*n elements")
+    if out is not None:
+        cap = out.shape[0]
+    elif cap is None:
+        cap = 16 * n + 1024
+    for _ in range(2):
+        buf = out if out is not None else torch.empty((cap, 2), dtype=torch.int32, device=w.device)
+        m = C.c_uint64(0)
+        st = Stats()
+        rc = _lib.girg_edges_shard(w.data_ptr(), x.data_ptr(), n, d, T, kappa, seed, shard[0], shard[1], shard[2],
+                                   buf.data_ptr(), cap, C.byref(m), C.byref(st) if stats else None,
+                                   _stream(stream))
+        if rc == ECAPACITY and out is None:
+            cap = int(m.value)
+            continue
+        _check(rc)
+        e = buf[: m.value]
+        return (e, st.as_dict()) if stats else e
+    raise GirgError(ECAPACITY)
+
+
+def edges_host(w_host, x_host, d: int, T: float, kappa: float, seed: int, out_host, stream=None) -> int:
+    """End-to-end call with HOST (ideally pinned) tensors: returns m; edges in out_host[:m]."""
+    n = w_host.numel()
+    m = C.c_uint64(0)
+    _check(_lib.girg_edges_host(w_host.data_ptr(), x_host.data_ptr(), n, d, T, kappa, seed, out_host.data_ptr(),
+                                out_host.shape[0], C.byref(m), _stream(stream)))
+    return int(m.value)
+
+
+def last_timings() -> dict:
+    """Phase timings (CUDA events on the call's stream) of this thread's last edges call."""
+    t = Timings()
+    _check(_lib.girg_last_timings(C.byref(t)))
+    return t.as_dict()
+
+
+def edge_keys(e: torch.Tensor) -> torch.Tensor:
+    """uint32 pairs as sorted int64 keys u*2^32+v (for set comparison)."""
+    u = e[:, 0].to(torch.int64) & 0xFFFFFFFF
+    v = e[:, 1].to(torch.int64) & 0xFFFFFFFF
+    return torch.sort(u * (1 << 32) + v).values

@@ -1,0 +1,1347 @@
+// girg.cu -- B200 (sm_100a) GIRG edge generator: kernels, host orchestration and the C ABI.
+//
+// Pipeline of girg_edges:
+//   K0 k_wstats     exact W (per-block 128-bit fixed point), weight-exponent histogram -> host plan
+//   H6 host plan    layers, CL / I levels, pbar tables
+//   K1 k_keys       layer + Morton cell at the insertion level, histogram over the cell space
+//   K2 k_scan_*     exclusive scan of the cell histogram = the prefix arrays P_C of Lemma 1
+//   K3 k_scatter    slot of every vertex in its cell
+//   K4 k_gather     in-cell order by vertex id (R11) + gather of x, w, id into sorted SoA
+//   K5 k_sample     per (layer pair, level, A cell): type-I pair tests and type-II geometric
+//                   jumps (Algorithm 1 events), warp-aggregated edge output
+// Citations "P:NNN" are lines of PAPER.md (arXiv:1905.06706); R* are DESIGN.md readings.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/girg.h"
+#include "girg_device.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace girg {
+
+constexpr int MAXL = 64;
+constexpr int EXP_BIAS = 1023;
+constexpr int HIST_BINS = 2048;
+constexpr int WS_THREADS = 256, WS_PER_THREAD = 8, WS_TILE = WS_THREADS * WS_PER_THREAD;
+
+// device error bits
+constexpr int ERR_WEIGHT = 1, ERR_WRANGE = 2, ERR_POS = 4, ERR_CHUNKS = 8;
+
+struct TabEntry {
+    double pbar;  // type-II bound for (i, j, level, class)
+    double Lbar;  // log1p(-pbar)
+    int clog2;    // chunk length C = 2^clog2 candidates
+    int pad;
+};
+
+struct Plan {
+    int L, d, e_min, maxCL;
+    double s, T, invT;
+    int sl, pad;
+    unsigned long long blo, bhi;
+    uint32_t base[MAXL + 1];    // offset of layer i in the concatenated cell space
+    uint32_t lstart[MAXL + 1];  // first sorted position of layer i
+    uint32_t cnt[MAXL];
+    uint8_t I[MAXL];
+    uint8_t CL[MAXL * MAXL];
+    uint32_t tab_off[MAXL * MAXL];
+};
+
+struct WPartial {
+    unsigned long long lo, hi;  // sum of m * 2^(e - e_b) over the block
+    int e_b, emax;
+    unsigned long long wmax_bits;  // largest weight of the block (positive doubles order as ints)
+};
+
+// ======================================================================================
+// H1, H2: generators
+// ======================================================================================
+__global__ void k_weights(uint32_t n, double ex, uint32_t k0, uint32_t k1, double* __restrict__ w)
+{
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const uint4 o = philox4x32_10(make_uint4(v, 0u, 0u, 1u), k0, k1);
+    const double U = u53(o.x, o.y);
+    w[v] = pow(__dsub_rn(1.0, U), ex);  // (1-U)^(-1/(beta-1)), 1-U exact
+}
+
+__global__ void k_positions(uint32_t n, int d, uint32_t k0, uint32_t k1, double* __restrict__ x)
+{
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    for (int k = 0; 2 * k < d; ++k) {
+        const uint4 o = philox4x32_10(make_uint4(v, (uint32_t)k, 0u, 2u), k0, k1);
+        x[(size_t)(2 * k) * n + v] = u53(o.x, o.y);
+        if (2 * k + 1 < d) x[(size_t)(2 * k + 1) * n + v] = u53(o.z, o.w);
+    }
+}
+
+// ======================================================================================
+// K0: weight statistics.  W exactly rounded (R3): w = m 2^(e-52) with m the 53-bit
+// significand; each block sums m * 2^(e - e_b) exactly in 128 bits (e_b = block minimum,
+// e - e_b <= 63 because at most 64 layers are allowed), the host adds the block partials in
+// 256 bits and rounds once.  Also the histogram of exponents (layer sizes).
+// ======================================================================================
+__device__ __forceinline__ void add128(unsigned long long& lo, unsigned long long& hi,
+                                       unsigned long long alo, unsigned long long ahi)
+{
+    const unsigned long long t = lo + alo;
+    hi += ahi + (t < lo ? 1ull : 0ull);
+    lo = t;
+}
+
+__global__ void __launch_bounds__(WS_THREADS) k_wstats(const double* __restrict__ w, uint32_t n,
+                                                       uint32_t* __restrict__ hist,
+                                                       WPartial* __restrict__ part,
+                                                       int* __restrict__ err)
+{
+    __shared__ uint32_t sh_hist[HIST_BINS];
+    __shared__ int sh_emin, sh_emax;
+    __shared__ unsigned long long sh_lo[WS_THREADS / 32], sh_hi[WS_THREADS / 32], sh_wmax;
+    for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x) sh_hist[i] = 0;
+    if (threadIdx.x == 0) { sh_emin = INT_MAX; sh_emax = INT_MIN; sh_wmax = 0; }
+    __syncthreads();
+
+    const size_t base = (size_t)blockIdx.x * WS_TILE;
+    unsigned long long m[WS_PER_THREAD];
+    int e[WS_PER_THREAD];
+    int emin = INT_MAX, emax = INT_MIN, bad = 0;
+    unsigned long long wmb = 0;
+#pragma unroll
+    for (int k = 0; k < WS_PER_THREAD; ++k) {
+        const size_t idx = base + (size_t)k * WS_THREADS + threadIdx.x;
+        e[k] = INT_MIN;
+        m[k] = 0;
+        if (idx < n) {
+            const unsigned long long bits = __double_as_longlong(w[idx]);
+            const int ef = (int)((bits >> 52) & 0x7ff);
+            const bool sign = (bits >> 63) != 0;
+            if (sign || ef == 0 || ef == 0x7ff) {  // <= 0, subnormal, inf, nan
+                bad |= ERR_WEIGHT;
+                continue;
+            }
+            const int ee = ef - EXP_BIAS;
+            if (ee < -500 || ee > 500) { bad |= ERR_WRANGE; continue; }
+            e[k] = ee;
+            m[k] = (bits & ((1ull << 52) - 1)) | (1ull << 52);
+            wmb = max(wmb, bits);
+            emin = min(emin, ee);
+            emax = max(emax, ee);
+            // warp-aggregated histogram update
+            const unsigned grp = __match_any_sync(__activemask(), ee);
+            if ((threadIdx.x & 31) == __ffs(grp) - 1) atomicAdd(&sh_hist[ee + EXP_BIAS], __popc(grp));
+        }
+    }
+    if (bad) atomicOr(err, bad);
+    atomicMin(&sh_emin, emin);
+    atomicMax(&sh_emax, emax);
+    atomicMax(&sh_wmax, wmb);
+    __syncthreads();
+    const int eb = sh_emin;
+    unsigned long long lo = 0, hi = 0;
+#pragma unroll
+    for (int k = 0; k < WS_PER_THREAD; ++k) {
+        if (e[k] == INT_MIN) continue;
+        const int sh = e[k] - eb;
+        if (sh > 63) { atomicOr(err, ERR_WRANGE); continue; }
+        const unsigned long long alo = m[k] << sh;
+        const unsigned long long ahi = sh ? (m[k] >> (64 - sh)) : 0ull;
+        add128(lo, hi, alo, ahi);
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        const unsigned long long olo = __shfl_down_sync(0xffffffffu, lo, off);
+        const unsigned long long ohi = __shfl_down_sync(0xffffffffu, hi, off);
+        add128(lo, hi, olo, ohi);
+    }
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { sh_lo[wid] = lo; sh_hi[wid] = hi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long tlo = 0, thi = 0;
+        for (int k = 0; k < WS_THREADS / 32; ++k) add128(tlo, thi, sh_lo[k], sh_hi[k]);
+        part[blockIdx.x].lo = tlo;
+        part[blockIdx.x].hi = thi;
+        part[blockIdx.x].e_b = eb;
+        part[blockIdx.x].emax = sh_emax;
+        part[blockIdx.x].wmax_bits = sh_wmax;
+    }
+    for (int i = threadIdx.x; i < HIST_BINS; i += blockDim.x)
+        if (sh_hist[i]) atomicAdd(&hist[i], sh_hist[i]);
+}
+
+// ======================================================================================
+// K1: cell keys at the insertion level (Lemma 1 proof P:994-996: coordinates by rounding,
+// Morton index P:577-588) over the concatenated cell space; histogram of keys.
+// ======================================================================================
+template <int D>
+__global__ void k_keys(const double* __restrict__ w, const double* __restrict__ x, uint32_t n,
+                       const Plan* __restrict__ pl, uint32_t* __restrict__ key,
+                       uint32_t* __restrict__ cnt, int* __restrict__ err)
+{
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const unsigned long long bits = __double_as_longlong(w[v]);
+    const int layer = (int)((bits >> 52) & 0x7ff) - EXP_BIAS - pl->e_min;
+    const int I = pl->I[layer];
+    const double scale = __ull2double_rn(1ull << I);
+    uint32_t c[D];
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const double xv = x[(size_t)k * n + v];
+        ok = ok && (xv >= 0.0) && (xv < 1.0);
+        c[k] = ok ? __double2uint_rz(__dmul_rn(xv, scale)) : 0u;
+    }
+    if (!ok) atomicOr(err, ERR_POS);
+    const uint32_t kv = pl->base[layer] + morton_encode<D>(c);
+    key[v] = kv;
+    atomicAdd(&cnt[kv], 1u);
+}
+
+// ======================================================================================
+// K2: exclusive scan of cnt[0..K] (K+1 entries) -> P (hand-written 3-phase scan)
+// ======================================================================================
+constexpr int SCAN_THREADS = 256, SCAN_PER_THREAD = 16, SCAN_TILE = SCAN_THREADS * SCAN_PER_THREAD;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* sh_warp, uint32_t& total)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += t;
+    }
+    if (lane == 31) sh_warp[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = blockDim.x >> 5;
+        uint32_t s = lane < nw ? sh_warp[lane] : 0u;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, s, off);
+            if (lane >= off) s += t;
+        }
+        if (lane < nw) sh_warp[lane] = s;
+    }
+    __syncthreads();
+    total = sh_warp[(blockDim.x >> 5) - 1];
+    const uint32_t wofs = wid ? sh_warp[wid - 1] : 0u;
+    __syncthreads();
+    return wofs + incl - v;
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_reduce(const uint32_t* __restrict__ in, uint64_t len,
+                                                              uint32_t* __restrict__ bsum)
+{
+    __shared__ uint32_t sh[SCAN_THREADS / 32];
+    const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE;
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+        const uint64_t i = base + (uint64_t)k * SCAN_THREADS + threadIdx.x;
+        if (i < len) s += in[i];
+    }
+    uint32_t total;
+    block_exclusive_scan(s, sh, total);
+    if (threadIdx.x == 0) bsum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_top(uint32_t* __restrict__ bsum, uint32_t nb)
+{
+    __shared__ uint32_t sh[32];
+    const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
+    uint32_t s = 0;
+    for (uint32_t b = b0; b < b1; ++b) s += bsum[b];
+    uint32_t total;
+    uint32_t ex = block_exclusive_scan(s, sh, total);
+    for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t t = bsum[b];
+        bsum[b] = ex;
+        ex += t;
+    }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const uint32_t* __restrict__ in, uint64_t len,
+                                                             const uint32_t* __restrict__ bsum,
+                                                             uint32_t* __restrict__ out)
+{
+    __shared__ uint32_t sh[SCAN_THREADS / 32];
+    // each thread owns SCAN_PER_THREAD consecutive elements
+    const uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_PER_THREAD;
+    uint32_t vals[SCAN_PER_THREAD];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+        const uint64_t i = base + k;
+        vals[k] = i < len ? in[i] : 0u;
+        s += vals[k];
+    }
+    uint32_t total;
+    uint32_t ex = block_exclusive_scan(s, sh, total) + bsum[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < SCAN_PER_THREAD; ++k) {
+        const uint64_t i = base + k;
+        if (i < len) out[i] = ex;
+        ex += vals[k];
+    }
+}
+
+// ======================================================================================
+// K3/K4: counting-sort placement; in-cell order by vertex id (R11) and payload gather
+// ======================================================================================
+__global__ void k_scatter(const uint32_t* __restrict__ key, uint32_t n, const uint32_t* __restrict__ P,
+                          uint32_t* __restrict__ cnt, uint32_t* __restrict__ tmp)
+{
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const uint32_t k = key[v];
+    const uint32_t slot = P[k] + atomicSub(&cnt[k], 1u) - 1u;
+    tmp[slot] = v;
+}
+
+template <int D>
+__global__ void k_gather(const uint32_t* __restrict__ tmp, const uint32_t* __restrict__ key, uint32_t n,
+                         const uint32_t* __restrict__ P, const double* __restrict__ w,
+                         const double* __restrict__ x, uint32_t* __restrict__ sid,
+                         uint32_t* __restrict__ skey, double* __restrict__ sw, double* __restrict__ sx)
+{
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const uint32_t v = tmp[s];
+    const uint32_t k = key[v];
+    const uint32_t lo = P[k], hi = P[k + 1];
+    uint32_t pos = s;
+    if (hi - lo > 1) {
+        uint32_t rank = 0;
+        for (uint32_t t = lo; t < hi; ++t) rank += tmp[t] < v;
+        pos = lo + rank;
+    }
+    sid[pos] = v;
+    skey[pos] = k;
+    sw[pos] = w[v];
+#pragma unroll
+    for (int c = 0; c < D; ++c) sx[(size_t)c * n + pos] = x[(size_t)c * n + v];
+}
+
+// ======================================================================================
+// K5: sampling
+// ======================================================================================
+struct Counters {
+    unsigned long long cand1, ev2, chunks, draws, landings, edges1, edges2, nt1, nt2;
+};
+
+struct SampleArgs {
+    const Plan* pl;
+    const TabEntry* tab;
+    const uint32_t* skey;
+    const double* sx;
+    const double* sw;
+    const uint32_t* sid;
+    const uint32_t* P;
+    uint32_t n;
+    uint32_t k0, k1;
+    uint2* edges;
+    unsigned long long cap;
+    unsigned long long* m;
+    Counters* stats;
+    int* err;
+};
+
+__device__ __forceinline__ void emit_edge(const SampleArgs& a, uint32_t u, uint32_t v)
+{
+    cg::coalesced_group g = cg::coalesced_threads();
+    unsigned long long slot = 0;
+    if (g.thread_rank() == 0) slot = atomicAdd(a.m, (unsigned long long)g.size());
+    slot = g.shfl(slot, 0) + g.thread_rank();
+    if (slot < a.cap) a.edges[slot] = make_uint2(min(u, v), max(u, v));
+}
+
+template <int D>
+__device__ __forceinline__ void load_point(const SampleArgs& a, uint32_t p, double (&xp)[D])
+{
+#pragma unroll
+    for (int k = 0; k < D; ++k) xp[k] = __ldg(&a.sx[(size_t)k * a.n + p]);
+}
+
+// V_i^A at level l (Lemma 1): [P_{C_1}, P_{C_{j+1}}) in sorted positions
+__device__ __forceinline__ void vrange(const SampleArgs& a, int i, uint32_t A, int l, uint32_t& lo, uint32_t& hi)
+{
+    const Plan* pl = a.pl;
+    const int sh = pl->d * ((int)pl->I[i] - l);
+    const uint32_t b = pl->base[i];
+    lo = __ldg(&a.P[b + (A << sh)]);
+    hi = __ldg(&a.P[b + ((A + 1u) << sh)]);
+}
+
+// Alg. 1 line 3 on V_i^A x V_j^B; same == (i == j && A == B) -> s < t (App. B.1)
+template <int D>
+__device__ void type1_event(const SampleArgs& a, uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1,
+                            bool same, Counters& c)
+{
+    const double s = a.pl->s, invT = a.pl->invT;
+    const bool thresh = a.pl->T == 0.0;
+    for (uint32_t sa = a0; sa < a1; ++sa) {
+        double xu[D];
+        load_point<D>(a, sa, xu);
+        const double wu = __ldg(&a.sw[sa]);
+        const uint32_t u = __ldg(&a.sid[sa]);
+        for (uint32_t tb = same ? sa + 1 : b0; tb < b1; ++tb) {
+            double xv[D];
+            load_point<D>(a, tb, xv);
+            const double wv = __ldg(&a.sw[tb]);
+            const uint32_t v = __ldg(&a.sid[tb]);
+            const double Dp = dist_pow<D>(xu, xv);
+            ++c.cand1;
+            bool edge;
+            if (thresh) {
+                edge = Dp <= __dmul_rn(__dmul_rn(wu, wv), s);
+            } else {
+                const double p = prob_uv(wu, wv, s, Dp, invT);
+                if (p >= 1.0) {
+                    edge = true;
+                } else {
+                    const uint4 o = philox4x32_10(make_uint4(min(u, v), max(u, v), 0u, 3u), a.k0, a.k1);
+                    const double r = u53(o.x, o.y);
+                    c.nt1 += fabs(r - p) < 1e-12;
+                    edge = r < p;
+                }
+            }
+            if (edge) {
+                ++c.edges1;
+                emit_edge(a, u, v);
+            }
+        }
+    }
+}
+
+// Alg. 1 lines 5-6, Sec. 4.2: chunked geometric jumps over the
+// row-major candidates of V_i^A x V_j^B, acceptance r_acc * pbar < p_uv (R10, R14).
+template <int D>
+__device__ void type2_event(const SampleArgs& a, uint32_t A, uint32_t B, int l, int i, int j,
+                            const TabEntry& te, uint32_t a0, uint32_t nA, uint32_t b0, uint32_t nB,
+                            Counters& c)
+{
+    const double s = a.pl->s, invT = a.pl->invT;
+    const unsigned long long N = (unsigned long long)nA * nB;
+    // R10: chunk length 2^clog2, doubled until the event has at most 2^15 chunks
+    int cl2 = te.clog2;
+    while (((N - 1) >> cl2) >= (1ull << 15)) ++cl2;
+    const unsigned long long C = 1ull << cl2;
+    const unsigned long long nch = (N - 1) / C + 1;
+    ++c.ev2;
+    const uint32_t tag = (uint32_t)l | ((uint32_t)i << 5) | ((uint32_t)j << 11);
+    for (unsigned long long ch = 0; ch < nch; ++ch) {
+        ++c.chunks;
+        const unsigned long long start = ch * C;
+        const long long end = (long long)min(N, start + C);
+        long long pos = (long long)start - 1;
+        for (uint32_t k = 0;; ++k) {
+            const uint4 o = philox4x32_10(make_uint4(A, B, tag | ((uint32_t)ch << 17), k), a.k0, a.k1);
+            ++c.draws;
+            const double rj = u53(o.x, o.y), ra = u53(o.z, o.w);
+            const double z = te.pbar == 1.0 ? 0.0 : __ddiv_rn(log(__dsub_rn(1.0, rj)), te.Lbar);
+            const long long remaining = end - pos - 1;
+            if (z >= (double)remaining) break;
+            pos += 1 + (long long)z;
+            ++c.landings;
+            const uint32_t sidx = (uint32_t)((unsigned long long)pos / nB);
+            const uint32_t tidx = (uint32_t)((unsigned long long)pos - (unsigned long long)sidx * nB);
+            const uint32_t pa = a0 + sidx, pb = b0 + tidx;
+            double xu[D], xv[D];
+            load_point<D>(a, pa, xu);
+            load_point<D>(a, pb, xv);
+            const double p = prob_uv(__ldg(&a.sw[pa]), __ldg(&a.sw[pb]), s, dist_pow<D>(xu, xv), invT);
+            const double rp = __dmul_rn(ra, te.pbar);
+            c.nt2 += fabs(rp - p) < 1e-12 * te.pbar;
+            if (rp < p) {
+                ++c.edges2;
+                emit_edge(a, __ldg(&a.sid[pa]), __ldg(&a.sid[pb]));
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ bool owned(const Plan* pl, int l, uint32_t A)
+{
+    const int d = pl->d;
+    const unsigned long long b = l >= pl->sl ? ((unsigned long long)A >> (d * (l - pl->sl)))
+                                             : ((unsigned long long)A << (d * (pl->sl - l)));
+    return b >= pl->blo && b < pl->bhi;
+}
+
+// one thread per sorted point p: p owns every cell A (of its layer i, at level l >= lf) of
+// which it is the first point; for each partner layer j >= i it processes the Algorithm-1
+// events with A on the i side (R16: i <= j; i == j -> A <= B, A < B for distant pairs).
+template <int D>
+__global__ void __launch_bounds__(256) k_sample(SampleArgs a)
+{
+    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= a.n) return;
+    const Plan* pl = a.pl;
+    const int L = pl->L;
+    int i = 0;
+    {
+        int lo = 0, hi = L - 1;  // last layer with lstart <= p
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pl->lstart[mid] <= p) lo = mid;
+            else hi = mid - 1;
+        }
+        i = lo;
+    }
+    const uint32_t code = __ldg(&a.skey[p]) - pl->base[i];
+    const int Ii = pl->I[i];
+    int lf = 0;  // coarsest level at which p is the first point of its cell
+    if (p != pl->lstart[i]) {
+        const uint32_t xr = code ^ (__ldg(&a.skey[p - 1]) - pl->base[i]);
+        if (xr == 0) return;
+        const int h = 31 - __clz(xr);
+        lf = Ii - h / D;
+    }
+    Counters c = {};
+    const bool binom = pl->T > 0.0;
+    for (int j = i; j < L; ++j) {
+        if (pl->cnt[j] == 0) continue;
+        const int cl = pl->CL[i * MAXL + j];
+        if (lf > cl) continue;
+        // ---------------- type-I at the comparison level ----------------
+        {
+            const int l = cl;
+            const uint32_t A = code >> (D * (Ii - l));
+            if (owned(pl, l, A)) {
+                uint32_t a0, a1;
+                vrange(a, i, A, l, a0, a1);
+                uint32_t ac[D];
+                morton_decode<D>(A, ac);
+                const uint32_t mask = (l >= 1) ? ((1u << l) - 1u) : 0u;
+                if (l <= 1) {
+                    for (uint32_t B = 0; B < (1u << (D * l)); ++B) {
+                        if (i == j && B < A) continue;
+                        uint32_t b0, b1;
+                        vrange(a, j, B, l, b0, b1);
+                        if (b1 > b0) type1_event<D>(a, a0, a1, b0, b1, i == j && A == B, c);
+                    }
+                } else {
+                    int off[D];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) off[k] = -1;
+                    while (true) {
+                        uint32_t bc[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) bc[k] = (ac[k] + (uint32_t)off[k]) & mask;
+                        const uint32_t B = morton_encode<D>(bc);
+                        if (!(i == j && B < A)) {
+                            uint32_t b0, b1;
+                            vrange(a, j, B, l, b0, b1);
+                            if (b1 > b0) type1_event<D>(a, a0, a1, b0, b1, i == j && A == B, c);
+                        }
+                        int k = 0;
+                        while (k < D && off[k] == 1) { off[k] = -1; ++k; }
+                        if (k == D) break;
+                        ++off[k];
+                    }
+                }
+            }
+        }
+        if (!binom) continue;
+        // ---------------- type-II at levels max(lf,2) .. CL (R2) ----------------
+        for (int l = max(lf, 2); l <= cl; ++l) {
+            const uint32_t A = code >> (D * (Ii - l));
+            if (!owned(pl, l, A)) continue;
+            uint32_t a0, a1;
+            vrange(a, i, A, l, a0, a1);
+            const uint32_t nA = a1 - a0;
+            uint32_t ac[D];
+            morton_decode<D>(A, ac);
+            const uint32_t mask = (1u << l) - 1u;
+            const TabEntry* te0 = a.tab + pl->tab_off[i * MAXL + j] + 2 * (l - 2);
+            if (l == 2) {
+                for (uint32_t B = 0; B < (1u << (2 * D)); ++B) {
+                    if (i == j && B <= A) continue;
+                    uint32_t bc[D];
+                    morton_decode<D>(B, bc);
+                    int dm = 0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) {
+                        const int g = abs((int)bc[k] - (int)ac[k]);
+                        dm = max(dm, min(g, 4 - g));
+                    }
+                    if (dm <= 1) continue;
+                    uint32_t b0, b1;
+                    vrange(a, j, B, l, b0, b1);
+                    if (b1 == b0) continue;
+                    const TabEntry te = te0[dm - 2];
+                    if (te.pbar == 0.0) continue;
+                    type2_event<D>(a, A, B, l, i, j, te, a0, nA, b0, b1 - b0, c);
+                }
+            } else {
+                int off[D], lo_[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    lo_[k] = -2 - (int)(ac[k] & 1u);
+                    off[k] = lo_[k];
+                }
+                while (true) {
+                    int dm = 0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) dm = max(dm, abs(off[k]));
+                    if (dm >= 2) {
+                        uint32_t bc[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) bc[k] = (ac[k] + (uint32_t)off[k]) & mask;
+                        const uint32_t B = morton_encode<D>(bc);
+                        if (!(i == j && B <= A)) {
+                            uint32_t b0, b1;
+                            vrange(a, j, B, l, b0, b1);
+                            if (b1 > b0) {
+                                const TabEntry te = te0[dm - 2];
+                                if (te.pbar != 0.0) type2_event<D>(a, A, B, l, i, j, te, a0, nA, b0, b1 - b0, c);
+                            }
+                        }
+                    }
+                    int k = 0;
+                    while (k < D && off[k] == lo_[k] + 5) { off[k] = lo_[k]; ++k; }
+                    if (k == D) break;
+                    ++off[k];
+                }
+            }
+        }
+    }
+    if (a.stats) {
+        atomicAdd(&a.stats->cand1, c.cand1);
+        atomicAdd(&a.stats->ev2, c.ev2);
+        atomicAdd(&a.stats->chunks, c.chunks);
+        atomicAdd(&a.stats->draws, c.draws);
+        atomicAdd(&a.stats->landings, c.landings);
+        atomicAdd(&a.stats->edges1, c.edges1);
+        atomicAdd(&a.stats->edges2, c.edges2);
+        atomicAdd(&a.stats->nt1, c.nt1);
+        atomicAdd(&a.stats->nt2, c.nt2);
+    }
+}
+
+// ======================================================================================
+// Host side
+// ======================================================================================
+thread_local std::string g_last_cuda;
+thread_local girg_timings g_timings;
+
+// CUDA events around the phases of one call (recorded on the call's stream)
+struct PhaseEvents {
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    PhaseEvents()
+    {
+        for (auto& e : ev) cudaEventCreate(&e);
+    }
+    ~PhaseEvents()
+    {
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+    void record(int k, cudaStream_t st) { cudaEventRecord(ev[k], st); }
+    double ms(int a, int b) const
+    {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, ev[a], ev[b]);
+        return (double)t;
+    }
+};
+
+struct CudaFail {
+    cudaError_t e;
+};
+
+#define GCHECK(x)                                  \
+    do {                                           \
+        cudaError_t e_ = (x);                      \
+        if (e_ != cudaSuccess) throw CudaFail{e_}; \
+    } while (0)
+
+static void pool_keep(int dev)
+{
+    static bool done[64] = {};
+    if (dev < 64 && !done[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        done[dev] = true;
+    }
+}
+
+// stream-ordered scratch allocations released in the destructor
+struct Scratch {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t s) : st(s)
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        pool_keep(dev);
+    }
+    template <class T>
+    T* alloc(size_t count)
+    {
+        void* p = nullptr;
+        const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+        cudaError_t e = cudaMallocAsync(&p, bytes, st);
+        if (e == cudaErrorMemoryAllocation) throw CudaFail{e};
+        GCHECK(e);
+        ptrs.push_back(p);
+        return (T*)p;
+    }
+    ~Scratch()
+    {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+    }
+};
+
+static inline unsigned grid_for(uint64_t n, unsigned threads) { return (unsigned)((n + threads - 1) / threads); }
+
+// round a 256-bit non-negative integer (4 x u64, little endian) times 2^e2 to double (RNE)
+static double round_u256(const unsigned long long a[4], int e2)
+{
+    int top = -1;
+    for (int k = 3; k >= 0 && top < 0; --k)
+        if (a[k]) top = 64 * k + 63 - __builtin_clzll(a[k]);
+    if (top < 0) return 0.0;
+    auto bit = [&](int i) -> unsigned { return i < 0 ? 0u : (unsigned)((a[i / 64] >> (i % 64)) & 1ull); };
+    unsigned long long mant = 0;
+    const int lo = std::max(0, top - 52);
+    for (int b = top; b >= lo; --b) mant = (mant << 1) | bit(b);
+    if (top <= 52) return std::ldexp((double)mant, e2);
+    const unsigned rnd = bit(top - 53);
+    bool sticky = false;
+    for (int b = top - 54; b >= 0 && !sticky; --b) sticky = bit(b) != 0;
+    int t = top;
+    if (rnd && (sticky || (mant & 1ull))) {
+        ++mant;
+        if (mant == (1ull << 53)) { mant >>= 1; ++t; }
+    }
+    return std::ldexp((double)mant, t - 52 + e2);
+}
+
+// exact W = sum_b part_b * 2^(e_b - 52), rounded once (R3)
+static double exact_W(const std::vector<WPartial>& parts, int emin)
+{
+    unsigned long long acc[4] = {0, 0, 0, 0};
+    for (const WPartial& q : parts) {
+        if (q.e_b == INT_MAX) continue;  // empty block
+        const int sh = q.e_b - emin;       // 0..63
+        unsigned long long v[4] = {0, 0, 0, 0};
+        if (sh == 0) {
+            v[0] = q.lo; v[1] = q.hi;
+        } else {
+            v[0] = q.lo << sh;
+            v[1] = (q.hi << sh) | (q.lo >> (64 - sh));
+            v[2] = q.hi >> (64 - sh);
+        }
+        unsigned long long carry = 0;
+        for (int k = 0; k < 4; ++k) {
+            const unsigned long long s1 = acc[k] + v[k];
+            const unsigned long long c1 = s1 < acc[k];
+            const unsigned long long s2 = s1 + carry;
+            const unsigned long long c2 = s2 < s1;
+            acc[k] = s2;
+            carry = c1 + c2;
+        }
+    }
+    return round_u256(acc, emin - 52);
+}
+
+struct HostPlan {
+    Plan p;
+    std::vector<TabEntry> tab;
+    uint64_t K = 0;
+    double W = 0;
+};
+
+// H6: layers, levels and bound tables; R5-R7, R9, R10.
+static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WPartial>& parts, uint64_t n, int d,
+                     double T, double kappa, HostPlan& hp)
+{
+    Plan& p = hp.p;
+    std::memset(&p, 0, sizeof(p));
+    int emin = INT_MAX, emax = INT_MIN;
+    for (int b = 0; b < HIST_BINS; ++b)
+        if (hist[b]) {
+            emin = std::min(emin, b - EXP_BIAS);
+            emax = std::max(emax, b - EXP_BIAS);
+        }
+    if (emin == INT_MAX) return GIRG_EINVAL;
+    if (emax - emin + 1 > MAXL) return GIRG_ERANGE;
+    hp.W = exact_W(parts, emin);
+    p.L = emax - emin + 1;
+    p.d = d;
+    p.e_min = emin;
+    p.T = T;
+    p.invT = T > 0.0 ? 1.0 / T : 0.0;
+    p.s = kappa / hp.W;
+    for (int i = 0; i < p.L; ++i) p.cnt[i] = hist[emin + i + EXP_BIAS];
+    int Ln = 0;
+    while (std::ldexp(1.0, d * Ln) < (double)n) ++Ln;
+    const int Lmax = std::min(Ln + 1, 32 / d);
+    int maxCL = 0;
+    for (int i = 0; i < p.L; ++i)
+        for (int j = 0; j < p.L; ++j) {
+            const double qbar = std::ldexp(1.0, 2 * emin + i + j + 2) * p.s;
+            int cl = 0;
+            for (int l = Lmax; l >= 0; --l)
+                if (std::ldexp(1.0, -d * l) >= qbar) { cl = l; break; }
+            p.CL[i * MAXL + j] = (uint8_t)cl;
+        }
+    for (int i = 0; i < p.L; ++i) {
+        int I = 0;
+        if (p.cnt[i])
+            for (int j = 0; j < p.L; ++j)
+                if (p.cnt[j]) {
+                    I = std::max(I, (int)p.CL[i * MAXL + j]);
+                    maxCL = std::max(maxCL, (int)p.CL[i * MAXL + j]);
+                }
+        if (d * I > 31) return GIRG_ERANGE;
+        p.I[i] = (uint8_t)I;
+    }
+    p.maxCL = maxCL;
+    uint64_t K = 0, ls = 0;
+    for (int i = 0; i < p.L; ++i) {
+        p.base[i] = (uint32_t)K;
+        p.lstart[i] = (uint32_t)ls;
+        K += 1ull << (d * p.I[i]);
+        ls += p.cnt[i];
+        if (K >= 0xFFFFFFFFull) return GIRG_ERANGE;
+    }
+    p.base[p.L] = (uint32_t)K;
+    p.lstart[p.L] = (uint32_t)ls;
+    hp.K = K;
+    hp.tab.clear();
+    if (T > 0.0) {
+        for (int i = 0; i < p.L; ++i)
+            for (int j = i; j < p.L; ++j) {
+                const int cl = p.CL[i * MAXL + j];
+                p.tab_off[i * MAXL + j] = (uint32_t)hp.tab.size();
+                if (!p.cnt[i] || !p.cnt[j] || cl < 2) continue;
+                const double qbar = std::ldexp(1.0, 2 * emin + i + j + 2) * p.s;
+                for (int l = 2; l <= cl; ++l)
+                    for (int k = 0; k < 2; ++k) {
+                        const double mind_d = std::ldexp(1.0, -d * l + d * k);  // ((k+1) 2^-l)^d
+                        const double ratio = qbar / mind_d;
+                        TabEntry e;
+                        e.pbar = ratio >= 1.0 ? 1.0 : std::pow(ratio, p.invT);
+                        e.Lbar = std::log1p(-e.pbar);
+                        int c2 = 0;
+                        if (e.pbar > 0.0) c2 = std::min(62, std::max(0, 1 - std::ilogb(e.pbar)));
+                        e.clog2 = c2;
+                        e.pad = 0;
+                        hp.tab.push_back(e);
+                    }
+            }
+    }
+    if (hp.tab.empty()) hp.tab.push_back(TabEntry{0, 0, 0, 0});
+    return GIRG_OK;
+}
+
+static int map_cuda(cudaError_t e)
+{
+    g_last_cuda = cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? GIRG_ENOMEM : GIRG_ECUDA;
+}
+
+// K0 on the device + D2H of the histogram and partials (one synchronisation)
+static void run_wstats(const double* w, uint64_t n, cudaStream_t st, Scratch& S, std::vector<uint32_t>& hist,
+                       std::vector<WPartial>& parts, int& err_host)
+{
+    const unsigned nb = grid_for(n, WS_TILE);
+    const size_t bytes = HIST_BINS * sizeof(uint32_t) + nb * sizeof(WPartial) + 16;
+    char* buf = S.alloc<char>(bytes);
+    uint32_t* d_hist = (uint32_t*)buf;
+    int* d_err = (int*)(buf + HIST_BINS * sizeof(uint32_t));
+    WPartial* d_part = (WPartial*)(buf + HIST_BINS * sizeof(uint32_t) + 16);
+    GCHECK(cudaMemsetAsync(buf, 0, HIST_BINS * sizeof(uint32_t) + 16, st));
+    k_wstats<<<nb, WS_THREADS, 0, st>>>(w, (uint32_t)n, d_hist, d_part, d_err);
+    GCHECK(cudaGetLastError());
+    std::vector<char> h(bytes);
+    GCHECK(cudaMemcpyAsync(h.data(), buf, bytes, cudaMemcpyDeviceToHost, st));
+    GCHECK(cudaStreamSynchronize(st));
+    hist.assign((uint32_t*)h.data(), (uint32_t*)h.data() + HIST_BINS);
+    std::memcpy(&err_host, h.data() + HIST_BINS * sizeof(uint32_t), sizeof(int));
+    parts.resize(nb);
+    std::memcpy(parts.data(), h.data() + HIST_BINS * sizeof(uint32_t) + 16, nb * sizeof(WPartial));
+}
+
+template <int D>
+static void launch_index(const double* w, const double* x, uint32_t n, const Plan* d_plan, uint64_t K,
+                         uint32_t* key, uint32_t* cnt, uint32_t* P, uint32_t* bsum, uint32_t* tmp, uint32_t* sid,
+                         uint32_t* skey, double* sw, double* sx, int* d_err, cudaStream_t st)
+{
+    const uint64_t len = K + 1;
+    GCHECK(cudaMemsetAsync(cnt, 0, len * sizeof(uint32_t), st));
+    k_keys<D><<<grid_for(n, 256), 256, 0, st>>>(w, x, n, d_plan, key, cnt, d_err);
+    const unsigned nb = grid_for(len, SCAN_TILE);
+    k_scan_reduce<<<nb, SCAN_THREADS, 0, st>>>(cnt, len, bsum);
+    k_scan_top<<<1, 1024, 0, st>>>(bsum, nb);
+    k_scan_final<<<nb, SCAN_THREADS, 0, st>>>(cnt, len, bsum, P);
+    k_scatter<<<grid_for(n, 256), 256, 0, st>>>(key, n, P, cnt, tmp);
+    k_gather<D><<<grid_for(n, 256), 256, 0, st>>>(tmp, key, n, P, w, x, sid, skey, sw, sx);
+    GCHECK(cudaGetLastError());
+}
+
+template <int D>
+static void launch_sample(const SampleArgs& a, cudaStream_t st)
+{
+    k_sample<D><<<grid_for(a.n, 256), 256, 0, st>>>(a);
+    GCHECK(cudaGetLastError());
+}
+
+static int edges_impl(const double* w, const double* x, uint64_t n, int d, double T, double kappa,
+                      uint64_t seed, int sl, uint64_t blo, uint64_t bhi, uint32_t* edges, uint64_t cap,
+                      uint64_t* m_out, girg_stats* stats_out, cudaStream_t st)
+{
+    if (!w || !x || !m_out || (cap && !edges)) return GIRG_EINVAL;
+    if (n == 0 || n >= (1ull << 32) || d < 1 || d > 5) return GIRG_EINVAL;
+    if (!(T >= 0.0 && T < 1.0) || !(kappa > 0.0) || !std::isfinite(kappa)) return GIRG_EINVAL;
+    if (sl < 0 || sl * d > 32 || blo >= bhi) return GIRG_EINVAL;
+    try {
+        PhaseEvents PE;
+        Scratch S(st);
+        std::vector<uint32_t> hist;
+        std::vector<WPartial> parts;
+        int herr = 0;
+        PE.record(0, st);
+        run_wstats(w, n, st, S, hist, parts, herr);
+        if (herr & ERR_WEIGHT) return GIRG_EINVAL;
+        if (herr & ERR_WRANGE) return GIRG_ERANGE;
+        HostPlan hp;
+        int rc = make_plan(hist, parts, n, d, T, kappa, hp);
+        if (rc) return rc;
+        hp.p.sl = sl;
+        hp.p.blo = blo;
+        hp.p.bhi = bhi;
+        const uint32_t n32 = (uint32_t)n;
+        const uint64_t K = hp.K;
+        // scratch
+        Plan* d_plan = S.alloc<Plan>(1);
+        TabEntry* d_tab = S.alloc<TabEntry>(hp.tab.size());
+        char* misc = S.alloc<char>(256);
+        int* d_err = (int*)misc;
+        unsigned long long* d_m = (unsigned long long*)(misc + 16);
+        Counters* d_cnt = (Counters*)(misc + 32);
+        uint32_t* key = S.alloc<uint32_t>(n);
+        uint32_t* tmp = S.alloc<uint32_t>(n);
+        uint32_t* cnt = S.alloc<uint32_t>(K + 1);
+        uint32_t* P = S.alloc<uint32_t>(K + 1);
+        uint32_t* bsum = S.alloc<uint32_t>(grid_for(K + 1, SCAN_TILE) + 1);
+        uint32_t* sid = S.alloc<uint32_t>(n);
+        uint32_t* skey = S.alloc<uint32_t>(n);
+        double* sw = S.alloc<double>(n);
+        double* sx = S.alloc<double>((size_t)d * n);
+        GCHECK(cudaMemcpyAsync(d_plan, &hp.p, sizeof(Plan), cudaMemcpyHostToDevice, st));
+        GCHECK(cudaMemcpyAsync(d_tab, hp.tab.data(), hp.tab.size() * sizeof(TabEntry), cudaMemcpyHostToDevice, st));
+        GCHECK(cudaMemsetAsync(misc, 0, 256, st));
+        PE.record(1, st);
+        switch (d) {
+            case 1: launch_index<1>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, sid, skey, sw, sx, d_err, st); break;
+            case 2: launch_index<2>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, sid, skey, sw, sx, d_err, st); break;
+            case 3: launch_index<3>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, sid, skey, sw, sx, d_err, st); break;
+            case 4: launch_index<4>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, sid, skey, sw, sx, d_err, st); break;
+            default: launch_index<5>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, sid, skey, sw, sx, d_err, st); break;
+        }
+        SampleArgs a;
+        a.pl = d_plan;
+        a.tab = d_tab;
+        a.skey = skey;
+        a.sx = sx;
+        a.sw = sw;
+        a.sid = sid;
+        a.P = P;
+        a.n = n32;
+        a.k0 = (uint32_t)seed;
+        a.k1 = (uint32_t)(seed >> 32);
+        a.edges = (uint2*)edges;
+        a.cap = cap;
+        a.m = d_m;
+        a.stats = stats_out ? d_cnt : nullptr;
+        a.err = d_err;
+        PE.record(2, st);
+        switch (d) {
+            case 1: launch_sample<1>(a, st); break;
+            case 2: launch_sample<2>(a, st); break;
+            case 3: launch_sample<3>(a, st); break;
+            case 4: launch_sample<4>(a, st); break;
+            default: launch_sample<5>(a, st); break;
+        }
+        PE.record(3, st);
+        char hmisc[256];
+        GCHECK(cudaMemcpyAsync(hmisc, misc, 256, cudaMemcpyDeviceToHost, st));
+        GCHECK(cudaStreamSynchronize(st));
+        g_timings.ms_wstats = PE.ms(0, 1);
+        g_timings.ms_index = PE.ms(1, 2);
+        g_timings.ms_sample = PE.ms(2, 3);
+        g_timings.ms_total = PE.ms(0, 3);
+        g_timings.launches = 8;  // k_wstats, k_keys, 3 x scan, k_scatter, k_gather, k_sample
+        g_timings.n = n;
+        g_timings.key_space = K;
+        g_timings.d = d;
+        int derr;
+        unsigned long long m;
+        Counters hc;
+        std::memcpy(&derr, hmisc, sizeof(int));
+        std::memcpy(&m, hmisc + 16, sizeof(m));
+        std::memcpy(&hc, hmisc + 32, sizeof(hc));
+        g_timings.m = m;
+        if (derr & ERR_POS) return GIRG_EINVAL;
+        if (derr & ERR_CHUNKS) return GIRG_ERANGE;
+        *m_out = m;
+        if (stats_out) {
+            stats_out->cand1 = hc.cand1;
+            stats_out->ev2 = hc.ev2;
+            stats_out->chunks = hc.chunks;
+            stats_out->draws = hc.draws;
+            stats_out->landings = hc.landings;
+            stats_out->edges1 = hc.edges1;
+            stats_out->edges2 = hc.edges2;
+            stats_out->neartie1 = hc.nt1;
+            stats_out->neartie2 = hc.nt2;
+            stats_out->layers = (uint64_t)hp.p.L;
+            stats_out->key_space = K;
+        }
+        return m > cap ? GIRG_ECAPACITY : GIRG_OK;
+    } catch (const CudaFail& f) {
+        return map_cuda(f.e);
+    } catch (...) {
+        return GIRG_ENOMEM;
+    }
+}
+
+// ======================================================================================
+// Average-degree estimation (Sec. 5.1, App. B.2), boundary call, not
+// on the timed edge path.  Device: exact W and wmax (k_wstats), then one pass that sums over
+// the vertices with w <= tau (the tail, never saturated for the kappas tried) and compacts the
+// heavier candidates; host: the monotone search on f with E_R evaluated in O(|R|) over the
+// sorted candidates (same decomposition as DESIGN.md R12).
+// ======================================================================================
+constexpr int SUM_THREADS = 256;
+
+struct TailSums {
+    double s1, s2, z1, z2;  // sum w, sum w^2, sum (w/wmax)^(1/T), sum (w/wmax)^(2/T) over w <= tau
+};
+
+__global__ void __launch_bounds__(SUM_THREADS) k_wsums(const double* __restrict__ w, uint32_t n, double tau,
+                                                       double wmax, double invT, TailSums* __restrict__ part,
+                                                       double* __restrict__ cand, uint32_t* __restrict__ ncand,
+                                                       uint32_t cap)
+{
+    __shared__ double sh[4][SUM_THREADS / 32];
+    double a1 = 0, a2 = 0, b1 = 0, b2 = 0;
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const double wv = w[v];
+        if (wv <= tau) {
+            a1 += wv;
+            a2 += wv * wv;
+            if (invT > 0.0) {
+                const double z = pow(wv / wmax, invT);
+                b1 += z;
+                b2 += z * z;
+            }
+        } else {
+            const uint32_t k = atomicAdd(ncand, 1u);
+            if (k < cap) cand[k] = wv;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        a1 += __shfl_down_sync(0xffffffffu, a1, off);
+        a2 += __shfl_down_sync(0xffffffffu, a2, off);
+        b1 += __shfl_down_sync(0xffffffffu, b1, off);
+        b2 += __shfl_down_sync(0xffffffffu, b2, off);
+    }
+    const int wid = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { sh[0][wid] = a1; sh[1][wid] = a2; sh[2][wid] = b1; sh[3][wid] = b2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        TailSums t = {0, 0, 0, 0};
+        for (int k = 0; k < SUM_THREADS / 32; ++k) { t.s1 += sh[0][k]; t.s2 += sh[1][k]; t.z1 += sh[2][k]; t.z2 += sh[3][k]; }
+        part[blockIdx.x] = t;
+    }
+}
+
+struct Estimator {
+    uint64_t n;
+    int d;
+    double T, W, wmax, tau;
+    TailSums tail;                // fixed-order sum of the block partials
+    std::vector<double> cand;     // weights > tau, decreasing
+
+    // f(kappa); returns false if tau is not small enough for this kappa (R must lie in cand)
+    bool f(double kappa, double& out) const
+    {
+        const double a = std::ldexp(kappa, d) / W;
+        if ((a * tau) * wmax > 1.0) return false;
+        const double invT = T > 0.0 ? 1.0 / T : 0.0;
+        const double G = T > 0.0 ? std::pow(std::sqrt(a) * wmax, invT) : 0.0;
+        const size_t nc = cand.size();
+        // R = prefix of cand with (a w) wmax > 1
+        size_t nr = 0;
+        while (nr < nc && (a * cand[nr]) * wmax > 1.0) ++nr;
+        std::vector<double> zeta(nc), S1s(nr + 1), SPs(nr + 1);
+        for (size_t k = 0; k < nc; ++k) zeta[k] = T > 0.0 ? std::pow(cand[k] / wmax, invT) : 0.0;
+        double Wsmall = tail.s1, Zs = tail.z1, W2s = tail.s2, Z2s = tail.z2;
+        for (size_t k = nr; k < nc; ++k) {  // candidates outside R
+            Wsmall += cand[k];
+            W2s += cand[k] * cand[k];
+            Zs += zeta[k];
+            Z2s += zeta[k] * zeta[k];
+        }
+        S1s[nr] = 0.0;
+        SPs[nr] = 0.0;
+        for (size_t k = nr; k-- > 0;) {
+            S1s[k] = S1s[k + 1] + cand[k];
+            SPs[k] = SPs[k + 1] + zeta[k];
+        }
+        const double Wt = Wsmall + S1s[0], Zt = Zs + SPs[0];
+        // pairs (u outside R, any v != u): all non-E_R
+        double Lsum = Wt * Wsmall - W2s;
+        double Psum = Zt * Zs - Z2s;  // in units of G^2
+        double nER = 0.0;
+        size_t m = nr;
+        for (size_t t = 0; t < nr; ++t) {
+            while (m > 0 && !((a * cand[t]) * cand[m - 1] > 1.0)) --m;
+            const bool self = t < m;
+            nER += (double)(m - (self ? 1 : 0));
+            Lsum += cand[t] * (Wsmall + S1s[m] - (self ? 0.0 : cand[t]));
+            Psum += zeta[t] * (Zs + SPs[m] - (self ? 0.0 : zeta[t]));
+        }
+        const double tot = T == 0.0 ? a * Lsum + nER : (a * Lsum - T * (G * G) * Psum) / (1.0 - T) + nER;
+        out = tot / (double)n;
+        return std::isfinite(out);
+    }
+};
+
+static void estimator_tail(const double* w, uint64_t n, Estimator& E, cudaStream_t st)
+{
+    uint32_t cap = 1u << 16;
+    for (;;) {
+        Scratch S(st);
+        const unsigned nb = std::min<unsigned>(grid_for(n, SUM_THREADS), 148u * 8u);
+        TailSums* d_part = S.alloc<TailSums>(nb);
+        double* d_cand = S.alloc<double>(cap);
+        uint32_t* d_nc = S.alloc<uint32_t>(1);
+        GCHECK(cudaMemsetAsync(d_nc, 0, sizeof(uint32_t), st));
+        k_wsums<<<nb, SUM_THREADS, 0, st>>>(w, (uint32_t)n, E.tau, E.wmax, E.T > 0.0 ? 1.0 / E.T : 0.0, d_part,
+                                            d_cand, d_nc, cap);
+        GCHECK(cudaGetLastError());
+        std::vector<TailSums> hp(nb);
+        uint32_t nc = 0;
+        GCHECK(cudaMemcpyAsync(hp.data(), d_part, nb * sizeof(TailSums), cudaMemcpyDeviceToHost, st));
+        GCHECK(cudaMemcpyAsync(&nc, d_nc, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        GCHECK(cudaStreamSynchronize(st));
+        if (nc > cap) {
+            cap = nc;
+            continue;
+        }
+        E.cand.resize(nc);
+        if (nc) {
+            GCHECK(cudaMemcpyAsync(E.cand.data(), d_cand, nc * sizeof(double), cudaMemcpyDeviceToHost, st));
+            GCHECK(cudaStreamSynchronize(st));
+        }
+        std::sort(E.cand.begin(), E.cand.end(), [](double x, double y) { return x > y; });
+        E.tail = TailSums{0, 0, 0, 0};
+        for (const TailSums& t : hp) {
+            E.tail.s1 += t.s1; E.tail.s2 += t.s2; E.tail.z1 += t.z1; E.tail.z2 += t.z2;
+        }
+        return;
+    }
+}
+
+static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double T, double beta, double* kappa_out,
+                      cudaStream_t st)
+{
+    if (!w || !kappa_out || n < 2 || n >= (1ull << 32) || d < 1 || d > 5) return GIRG_EINVAL;
+    if (!(T >= 0.0 && T < 1.0) || !(beta > 2.0) || !std::isfinite(beta)) return GIRG_EINVAL;
+    if (!(avg_deg > 0.0 && avg_deg < (double)(n - 1))) return GIRG_EINVAL;
+    try {
+        Estimator E;
+        E.n = n;
+        E.d = d;
+        E.T = T;
+        {
+            Scratch S(st);
+            std::vector<uint32_t> hist;
+            std::vector<WPartial> parts;
+            int herr = 0;
+            run_wstats(w, n, st, S, hist, parts, herr);
+            if (herr & ERR_WEIGHT) return GIRG_EINVAL;
+            if (herr & ERR_WRANGE) return GIRG_ERANGE;
+            int emin = INT_MAX;
+            unsigned long long wb = 0;
+            for (const WPartial& q : parts)
+                if (q.e_b != INT_MAX) { emin = std::min(emin, q.e_b); wb = std::max(wb, q.wmax_bits); }
+            E.W = exact_W(parts, emin);
+            std::memcpy(&E.wmax, &wb, sizeof(double));
+        }
+        const double Ew = (beta - 1.0) / (beta - 2.0);
+        const double k0 = avg_deg * (1.0 - T) / (std::ldexp(1.0, d) * Ew);
+        auto set_tau = [&](double kappa) {
+            const double a = std::ldexp(kappa, d) / E.W;
+            E.tau = 0.25 / (a * E.wmax);
+            estimator_tail(w, n, E, st);
+        };
+        set_tau(k0);
+        auto f = [&](double kappa, double& out) -> bool {
+            for (int tries = 0; tries < 64; ++tries) {
+                if (E.f(kappa, out)) return true;
+                const double a = std::ldexp(kappa, d) / E.W;
+                if ((a * E.tau) * E.wmax <= 1.0) return false;  // non-finite value
+                set_tau(kappa);
+            }
+            return false;
+        };
+        double lo, hi, fv;
+        if (!f(k0, fv)) return GIRG_ERANGE;
+        int it = 0;
+        if (fv < avg_deg) {
+            lo = k0;
+            hi = 2.0 * k0;
+            for (;;) {
+                if (!f(hi, fv)) return GIRG_ERANGE;
+                if (!(fv < avg_deg)) break;
+                lo = hi;
+                hi *= 2.0;
+                if (++it > 2000) return GIRG_ERANGE;
+            }
+        } else {
+            hi = k0;
+            lo = 0.5 * k0;
+            for (;;) {
+                if (!f(lo, fv)) return GIRG_ERANGE;
+                if (fv < avg_deg) break;
+                hi = lo;
+                lo *= 0.5;
+                if (++it > 2000) return GIRG_ERANGE;
+            }
+        }
+        for (it = 0; it < 200 && hi / lo - 1.0 >= 1e-13; ++it) {
+            const double mid = std::sqrt(lo * hi);
+            if (!f(mid, fv)) return GIRG_ERANGE;
+            if (fv < avg_deg) lo = mid;
+            else hi = mid;
+        }
+        *kappa_out = 0.5 * (lo + hi);
+        return GIRG_OK;
+    } catch (const CudaFail& fl) {
+        return map_cuda(fl.e);
+    } catch (...) {
+        return GIRG_ENOMEM;
+    }
+}
+
+}  // namespace girg
+
+// ======================================================================================
+// C ABI
+// ======================================================================================
+using namespace girg;
+
+extern "C" int girg_weights(uint64_t n, double beta, uint64_t seed, double* w_dev, void* stream)
+{
+    if (n == 0 || n >= (1ull << 32) || !(beta > 2.0) || !std::isfinite(beta) || !w_dev) return GIRG_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_weights<<<grid_for(n, 256), 256, 0, st>>>((uint32_t)n, -1.0 / (beta - 1.0), (uint32_t)seed,
+                                                (uint32_t)(seed >> 32), w_dev);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GIRG_OK : map_cuda(e);
+}
+
+extern "C" int girg_positions(uint64_t n, int d, uint64_t seed, double* x_dev, void* stream)
+{
+    if (n == 0 || n >= (1ull << 32) || d < 1 || d > 5 || !x_dev) return GIRG_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_positions<<<grid_for(n, 256), 256, 0, st>>>((uint32_t)n, d, (uint32_t)seed, (uint32_t)(seed >> 32), x_dev);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? GIRG_OK : map_cuda(e);
+}
+
+extern "C" int girg_scale_weights(const double* w_dev, uint64_t n, double avg_deg, int d, double T, double beta,
+                                  double* kappa_out, void* stream)
+{
+    return scale_impl(w_dev, n, avg_deg, d, T, beta, kappa_out, (cudaStream_t)stream);
+}
+
+extern "C" int girg_edges(const double* w_dev, const double* x_dev, uint64_t n, int d, double T, double kappa,
+                          uint64_t seed, uint32_t* edges_dev, uint64_t cap, uint64_t* m_out, void* stream)
+{
+    return edges_impl(w_dev, x_dev, n, d, T, kappa, seed, 0, 0, 1, edges_dev, cap, m_out, nullptr,
+                      (cudaStream_t)stream);
+}
+
+extern "C" int girg_edges_shard(const double* w_dev, const double* x_dev, uint64_t n, int d, double T,
+                                double kappa, uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi,
+                                uint32_t* edges_dev, uint64_t cap, uint64_t* m_out, girg_stats* stats_out,
+                                void* stream)
+{
+    return edges_impl(w_dev, x_dev, n, d, T, kappa, seed, shard_level, blk_lo, blk_hi, edges_dev, cap, m_out,
+                      stats_out, (cudaStream_t)stream);
+}
+
+extern "C" int girg_edges_host(const double* w_host, const double* x_host, uint64_t n, int d, double T,
+                               double kappa, uint64_t seed, uint32_t* edges_host, uint64_t cap, uint64_t* m_out,
+                               void* stream)
+{
+    if (!w_host || !x_host || !m_out || (cap && !edges_host)) return GIRG_EINVAL;
+    if (n == 0 || n >= (1ull << 32) || d < 1 || d > 5) return GIRG_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    try {
+        Scratch S(st);
+        double* w = S.alloc<double>(n);
+        double* x = S.alloc<double>((size_t)d * n);
+        uint32_t* e = S.alloc<uint32_t>(2 * std::max<uint64_t>(cap, 1));
+        GCHECK(cudaMemcpyAsync(w, w_host, n * sizeof(double), cudaMemcpyHostToDevice, st));
+        GCHECK(cudaMemcpyAsync(x, x_host, (size_t)d * n * sizeof(double), cudaMemcpyHostToDevice, st));
+        int rc = edges_impl(w, x, n, d, T, kappa, seed, 0, 0, 1, e, cap, m_out, nullptr, st);
+        if (rc != GIRG_OK) return rc;
+        if (*m_out) GCHECK(cudaMemcpyAsync(edges_host, e, *m_out * 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        GCHECK(cudaStreamSynchronize(st));
+        return GIRG_OK;
+    } catch (const CudaFail& f) {
+        return map_cuda(f.e);
+    } catch (...) {
+        return GIRG_ENOMEM;
+    }
+}
+
+extern "C" const char* girg_strerror(int status)
+{
+    switch (status) {
+        case GIRG_OK: return "ok";
+        case GIRG_EINVAL: return "invalid argument";
+        case GIRG_ECAPACITY: return "edge buffer too small (m_out holds the required count)";
+        case GIRG_ERANGE: return "input outside the supported range of the index";
+        case GIRG_ENOMEM: return "out of device memory";
+        case GIRG_ECUDA: return "CUDA runtime error";
+        default: return "unknown status";
+    }
+}
+
+extern "C" int girg_last_timings(girg_timings* out)
+{
+    if (!out) return GIRG_EINVAL;
+    *out = girg::g_timings;
+    return GIRG_OK;
+}
+
+extern "C" const char* girg_last_cuda_error(void) { return girg::g_last_cuda.c_str(); }
+
+extern "C" int girg_version(void) { return 100; }

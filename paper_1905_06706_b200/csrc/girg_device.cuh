@@ -1,0 +1,142 @@
+// girg_device.cuh -- device primitives of the B200 GIRG generator (sm_100a).
+//
+// Philox4x32-10 counter-based randomness, 53-bit uniforms, Morton interleave and the canonical
+// double-precision model arithmetic (no FMA contraction: the library is compiled with
+// -fmad=false so every product and sum rounds separately, as in DESIGN.md "Canonical
+// arithmetic").  Citations "P:NNN" refer to lines of PAPER.md (arXiv:1905.06706).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace girg {
+
+// ---------------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11).  Key = (lo32(seed), hi32(seed)).  Each round is two
+// 32x32->64 multiplies (IMAD.WIDE / IMAD.HI) and two 3-input XORs (LOP3).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    }
+    return c;
+}
+
+// uniform on the 2^-53 grid in [0,1) from words (hi, lo): exact conversion
+__device__ __forceinline__ double u53(uint32_t hi, uint32_t lo)
+{
+    const unsigned long long b = ((((unsigned long long)hi) << 32) | lo) >> 11;
+    return __dmul_rn(__ull2double_rn(b), 0x1p-53);
+}
+
+// ---------------------------------------------------------------------------------------
+// Morton code: bit interleave, coordinate 0 most significant in each
+// d-bit group.  `lvl` bits per coordinate, d*lvl <= 31.
+// ---------------------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ uint32_t spread_bits(uint32_t c)
+{
+    if constexpr (D == 1) {
+        return c;
+    } else if constexpr (D == 2) {
+        c &= 0x0000ffffu;
+        c = (c | (c << 8)) & 0x00ff00ffu;
+        c = (c | (c << 4)) & 0x0f0f0f0fu;
+        c = (c | (c << 2)) & 0x33333333u;
+        c = (c | (c << 1)) & 0x55555555u;
+        return c;
+    } else if constexpr (D == 3) {
+        c &= 0x000003ffu;
+        c = (c | (c << 16)) & 0x030000ffu;
+        c = (c | (c << 8)) & 0x0300f00fu;
+        c = (c | (c << 4)) & 0x030c30c3u;
+        c = (c | (c << 2)) & 0x09249249u;
+        return c;
+    } else {
+        uint32_t r = 0;
+#pragma unroll
+        for (int b = 0; b < 32 / D; ++b) r |= ((c >> b) & 1u) << (b * D);
+        return r;
+    }
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t gather_bits(uint32_t m)
+{
+    if constexpr (D == 1) {
+        return m;
+    } else if constexpr (D == 2) {
+        m &= 0x55555555u;
+        m = (m | (m >> 1)) & 0x33333333u;
+        m = (m | (m >> 2)) & 0x0f0f0f0fu;
+        m = (m | (m >> 4)) & 0x00ff00ffu;
+        m = (m | (m >> 8)) & 0x0000ffffu;
+        return m;
+    } else if constexpr (D == 3) {
+        m &= 0x09249249u;
+        m = (m | (m >> 2)) & 0x030c30c3u;
+        m = (m | (m >> 4)) & 0x0300f00fu;
+        m = (m | (m >> 8)) & 0x030000ffu;
+        m = (m | (m >> 16)) & 0x000003ffu;
+        return m;
+    } else {
+        uint32_t r = 0;
+#pragma unroll
+        for (int b = 0; b < 32 / D; ++b) r |= ((m >> (b * D)) & 1u) << b;
+        return r;
+    }
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t morton_encode(const uint32_t (&c)[D])
+{
+    uint32_t code = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) code |= spread_bits<D>(c[k]) << (D - 1 - k);
+    return code;
+}
+
+template <int D>
+__device__ __forceinline__ void morton_decode(uint32_t code, uint32_t (&c)[D])
+{
+#pragma unroll
+    for (int k = 0; k < D; ++k) c[k] = gather_bits<D>(code >> (D - 1 - k));
+}
+
+// ---------------------------------------------------------------------------------------
+// Canonical model arithmetic: torus L-inf distance, D = dist^d left
+// to right, q = (w_u*w_v)*s, p = min(1, (q/D)^(1/T)) (Eq. 1 P:277 in kappa form), threshold
+// D <= q.
+// ---------------------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ double dist_pow(const double (&xu)[D], const double (&xv)[D])
+{
+    double dist = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const double a = fabs(__dsub_rn(xu[k], xv[k]));
+        const double t = fmin(a, __dsub_rn(1.0, a));
+        dist = fmax(dist, t);
+    }
+    double P = dist;
+#pragma unroll
+    for (int k = 1; k < D; ++k) P = __dmul_rn(P, dist);
+    return P;
+}
+
+__device__ __forceinline__ double prob_uv(double wu, double wv, double s, double Dp, double invT)
+{
+    const double q = __dmul_rn(__dmul_rn(wu, wv), s);
+    const double ratio = __ddiv_rn(q, Dp);
+    if (ratio >= 1.0) return 1.0;
+    return pow(ratio, invT);
+}
+
+}  // namespace girg
