@@ -19,6 +19,9 @@ import torch
 
 from ._build import LIB as _LIB_PATH
 
+if os.environ.get("GIRG_LIBRARY"):  # e.g. the bounds-checked libgirg_debug.so
+    _LIB_PATH = os.environ["GIRG_LIBRARY"]
+
 OK, EINVAL, ECAPACITY, ERANGE, ENOMEM, ECUDA = 0, -1, -2, -3, -4, -5
 
 if not os.path.exists(_LIB_PATH):

@@ -7,8 +7,10 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "girg.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", "girg_device.cuh"), os.path.join(ROOT, "include", "girg.h")]
+DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("girg_device.cuh", "sample.cuh")] + [
+    os.path.join(ROOT, "include", "girg.h")]
 LIB = os.path.join(HERE, "libgirg.so")
+DEBUG_LIB = os.path.join(HERE, "libgirg_debug.so")  # bounds-checked build (-DGIRG_DEBUG)
 
 NVCC_FLAGS = [
     "-O3",
@@ -28,16 +30,17 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(p) for p in DEPS)
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    lib = DEBUG_LIB if debug else LIB
+    stale = force or not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(p) for p in DEPS)
     if stale:
-        tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
+        tmp = lib + f".tmp{os.getpid()}"
+        cmd = [nvcc(), *NVCC_FLAGS, *(["-DGIRG_DEBUG"] if debug else []), "-o", tmp, *SOURCES]
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -18,6 +18,8 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -35,7 +37,7 @@ constexpr int HIST_BINS = 2048;
 constexpr int WS_THREADS = 256, WS_PER_THREAD = 8, WS_TILE = WS_THREADS * WS_PER_THREAD;
 
 // device error bits
-constexpr int ERR_WEIGHT = 1, ERR_WRANGE = 2, ERR_POS = 4, ERR_CHUNKS = 8;
+constexpr int ERR_WEIGHT = 1, ERR_WRANGE = 2, ERR_POS = 4;
 
 struct TabEntry {
     double pbar;  // type-II bound for (i, j, level, class)
@@ -55,6 +57,10 @@ struct Plan {
     uint8_t I[MAXL];
     uint8_t CL[MAXL * MAXL];
     uint32_t tab_off[MAXL * MAXL];
+    // enumeration task lists per (layer i, first level lf): entries j | l<<6
+    // in tasks[toff[k][i*32+lf] ...], tcnt[k][i*32+lf] entries; k = 0 type-I, 1 type-II
+    uint32_t toff[2][MAXL * 32];
+    uint16_t tcnt[2][MAXL * 32];
 };
 
 struct WPartial {
@@ -336,302 +342,8 @@ __global__ void k_gather(const uint32_t* __restrict__ tmp, const uint32_t* __res
     for (int c = 0; c < D; ++c) sx[(size_t)c * n + pos] = x[(size_t)c * n + v];
 }
 
-// ======================================================================================
-// K5: sampling
-// ======================================================================================
-struct Counters {
-    unsigned long long cand1, ev2, chunks, draws, landings, edges1, edges2, nt1, nt2;
-};
-
-struct SampleArgs {
-    const Plan* pl;
-    const TabEntry* tab;
-    const uint32_t* skey;
-    const double* sx;
-    const double* sw;
-    const uint32_t* sid;
-    const uint32_t* P;
-    uint32_t n;
-    uint32_t k0, k1;
-    uint2* edges;
-    unsigned long long cap;
-    unsigned long long* m;
-    Counters* stats;
-    int* err;
-};
-
-__device__ __forceinline__ void emit_edge(const SampleArgs& a, uint32_t u, uint32_t v)
-{
-    cg::coalesced_group g = cg::coalesced_threads();
-    unsigned long long slot = 0;
-    if (g.thread_rank() == 0) slot = atomicAdd(a.m, (unsigned long long)g.size());
-    slot = g.shfl(slot, 0) + g.thread_rank();
-    if (slot < a.cap) a.edges[slot] = make_uint2(min(u, v), max(u, v));
-}
-
-template <int D>
-__device__ __forceinline__ void load_point(const SampleArgs& a, uint32_t p, double (&xp)[D])
-{
-#pragma unroll
-    for (int k = 0; k < D; ++k) xp[k] = __ldg(&a.sx[(size_t)k * a.n + p]);
-}
-
-// V_i^A at level l (Lemma 1): [P_{C_1}, P_{C_{j+1}}) in sorted positions
-__device__ __forceinline__ void vrange(const SampleArgs& a, int i, uint32_t A, int l, uint32_t& lo, uint32_t& hi)
-{
-    const Plan* pl = a.pl;
-    const int sh = pl->d * ((int)pl->I[i] - l);
-    const uint32_t b = pl->base[i];
-    lo = __ldg(&a.P[b + (A << sh)]);
-    hi = __ldg(&a.P[b + ((A + 1u) << sh)]);
-}
-
-// Alg. 1 line 3 on V_i^A x V_j^B; same == (i == j && A == B) -> s < t (App. B.1)
-template <int D>
-__device__ void type1_event(const SampleArgs& a, uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1,
-                            bool same, Counters& c)
-{
-    const double s = a.pl->s, invT = a.pl->invT;
-    const bool thresh = a.pl->T == 0.0;
-    for (uint32_t sa = a0; sa < a1; ++sa) {
-        double xu[D];
-        load_point<D>(a, sa, xu);
-        const double wu = __ldg(&a.sw[sa]);
-        const uint32_t u = __ldg(&a.sid[sa]);
-        for (uint32_t tb = same ? sa + 1 : b0; tb < b1; ++tb) {
-            double xv[D];
-            load_point<D>(a, tb, xv);
-            const double wv = __ldg(&a.sw[tb]);
-            const uint32_t v = __ldg(&a.sid[tb]);
-            const double Dp = dist_pow<D>(xu, xv);
-            ++c.cand1;
-            bool edge;
-            if (thresh) {
-                edge = Dp <= __dmul_rn(__dmul_rn(wu, wv), s);
-            } else {
-                const double p = prob_uv(wu, wv, s, Dp, invT);
-                if (p >= 1.0) {
-                    edge = true;
-                } else {
-                    const uint4 o = philox4x32_10(make_uint4(min(u, v), max(u, v), 0u, 3u), a.k0, a.k1);
-                    const double r = u53(o.x, o.y);
-                    c.nt1 += fabs(r - p) < 1e-12;
-                    edge = r < p;
-                }
-            }
-            if (edge) {
-                ++c.edges1;
-                emit_edge(a, u, v);
-            }
-        }
-    }
-}
-
-// Alg. 1 lines 5-6, Sec. 4.2: chunked geometric jumps over the
-// row-major candidates of V_i^A x V_j^B, acceptance r_acc * pbar < p_uv (R10, R14).
-template <int D>
-__device__ void type2_event(const SampleArgs& a, uint32_t A, uint32_t B, int l, int i, int j,
-                            const TabEntry& te, uint32_t a0, uint32_t nA, uint32_t b0, uint32_t nB,
-                            Counters& c)
-{
-    const double s = a.pl->s, invT = a.pl->invT;
-    const unsigned long long N = (unsigned long long)nA * nB;
-    // R10: chunk length 2^clog2, doubled until the event has at most 2^15 chunks
-    int cl2 = te.clog2;
-    while (((N - 1) >> cl2) >= (1ull << 15)) ++cl2;
-    const unsigned long long C = 1ull << cl2;
-    const unsigned long long nch = (N - 1) / C + 1;
-    ++c.ev2;
-    const uint32_t tag = (uint32_t)l | ((uint32_t)i << 5) | ((uint32_t)j << 11);
-    for (unsigned long long ch = 0; ch < nch; ++ch) {
-        ++c.chunks;
-        const unsigned long long start = ch * C;
-        const long long end = (long long)min(N, start + C);
-        long long pos = (long long)start - 1;
-        for (uint32_t k = 0;; ++k) {
-            const uint4 o = philox4x32_10(make_uint4(A, B, tag | ((uint32_t)ch << 17), k), a.k0, a.k1);
-            ++c.draws;
-            const double rj = u53(o.x, o.y), ra = u53(o.z, o.w);
-            const double z = te.pbar == 1.0 ? 0.0 : __ddiv_rn(log(__dsub_rn(1.0, rj)), te.Lbar);
-            const long long remaining = end - pos - 1;
-            if (z >= (double)remaining) break;
-            pos += 1 + (long long)z;
-            ++c.landings;
-            const uint32_t sidx = (uint32_t)((unsigned long long)pos / nB);
-            const uint32_t tidx = (uint32_t)((unsigned long long)pos - (unsigned long long)sidx * nB);
-            const uint32_t pa = a0 + sidx, pb = b0 + tidx;
-            double xu[D], xv[D];
-            load_point<D>(a, pa, xu);
-            load_point<D>(a, pb, xv);
-            const double p = prob_uv(__ldg(&a.sw[pa]), __ldg(&a.sw[pb]), s, dist_pow<D>(xu, xv), invT);
-            const double rp = __dmul_rn(ra, te.pbar);
-            c.nt2 += fabs(rp - p) < 1e-12 * te.pbar;
-            if (rp < p) {
-                ++c.edges2;
-                emit_edge(a, __ldg(&a.sid[pa]), __ldg(&a.sid[pb]));
-            }
-        }
-    }
-}
-
-__device__ __forceinline__ bool owned(const Plan* pl, int l, uint32_t A)
-{
-    const int d = pl->d;
-    const unsigned long long b = l >= pl->sl ? ((unsigned long long)A >> (d * (l - pl->sl)))
-                                             : ((unsigned long long)A << (d * (pl->sl - l)));
-    return b >= pl->blo && b < pl->bhi;
-}
-
-// one thread per sorted point p: p owns every cell A (of its layer i, at level l >= lf) of
-// which it is the first point; for each partner layer j >= i it processes the Algorithm-1
-// events with A on the i side (R16: i <= j; i == j -> A <= B, A < B for distant pairs).
-template <int D>
-__global__ void __launch_bounds__(256) k_sample(SampleArgs a)
-{
-    const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= a.n) return;
-    const Plan* pl = a.pl;
-    const int L = pl->L;
-    int i = 0;
-    {
-        int lo = 0, hi = L - 1;  // last layer with lstart <= p
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (pl->lstart[mid] <= p) lo = mid;
-            else hi = mid - 1;
-        }
-        i = lo;
-    }
-    const uint32_t code = __ldg(&a.skey[p]) - pl->base[i];
-    const int Ii = pl->I[i];
-    int lf = 0;  // coarsest level at which p is the first point of its cell
-    if (p != pl->lstart[i]) {
-        const uint32_t xr = code ^ (__ldg(&a.skey[p - 1]) - pl->base[i]);
-        if (xr == 0) return;
-        const int h = 31 - __clz(xr);
-        lf = Ii - h / D;
-    }
-    Counters c = {};
-    const bool binom = pl->T > 0.0;
-    for (int j = i; j < L; ++j) {
-        if (pl->cnt[j] == 0) continue;
-        const int cl = pl->CL[i * MAXL + j];
-        if (lf > cl) continue;
-        // ---------------- type-I at the comparison level ----------------
-        {
-            const int l = cl;
-            const uint32_t A = code >> (D * (Ii - l));
-            if (owned(pl, l, A)) {
-                uint32_t a0, a1;
-                vrange(a, i, A, l, a0, a1);
-                uint32_t ac[D];
-                morton_decode<D>(A, ac);
-                const uint32_t mask = (l >= 1) ? ((1u << l) - 1u) : 0u;
-                if (l <= 1) {
-                    for (uint32_t B = 0; B < (1u << (D * l)); ++B) {
-                        if (i == j && B < A) continue;
-                        uint32_t b0, b1;
-                        vrange(a, j, B, l, b0, b1);
-                        if (b1 > b0) type1_event<D>(a, a0, a1, b0, b1, i == j && A == B, c);
-                    }
-                } else {
-                    int off[D];
-#pragma unroll
-                    for (int k = 0; k < D; ++k) off[k] = -1;
-                    while (true) {
-                        uint32_t bc[D];
-#pragma unroll
-                        for (int k = 0; k < D; ++k) bc[k] = (ac[k] + (uint32_t)off[k]) & mask;
-                        const uint32_t B = morton_encode<D>(bc);
-                        if (!(i == j && B < A)) {
-                            uint32_t b0, b1;
-                            vrange(a, j, B, l, b0, b1);
-                            if (b1 > b0) type1_event<D>(a, a0, a1, b0, b1, i == j && A == B, c);
-                        }
-                        int k = 0;
-                        while (k < D && off[k] == 1) { off[k] = -1; ++k; }
-                        if (k == D) break;
-                        ++off[k];
-                    }
-                }
-            }
-        }
-        if (!binom) continue;
-        // ---------------- type-II at levels max(lf,2) .. CL (R2) ----------------
-        for (int l = max(lf, 2); l <= cl; ++l) {
-            const uint32_t A = code >> (D * (Ii - l));
-            if (!owned(pl, l, A)) continue;
-            uint32_t a0, a1;
-            vrange(a, i, A, l, a0, a1);
-            const uint32_t nA = a1 - a0;
-            uint32_t ac[D];
-            morton_decode<D>(A, ac);
-            const uint32_t mask = (1u << l) - 1u;
-            const TabEntry* te0 = a.tab + pl->tab_off[i * MAXL + j] + 2 * (l - 2);
-            if (l == 2) {
-                for (uint32_t B = 0; B < (1u << (2 * D)); ++B) {
-                    if (i == j && B <= A) continue;
-                    uint32_t bc[D];
-                    morton_decode<D>(B, bc);
-                    int dm = 0;
-#pragma unroll
-                    for (int k = 0; k < D; ++k) {
-                        const int g = abs((int)bc[k] - (int)ac[k]);
-                        dm = max(dm, min(g, 4 - g));
-                    }
-                    if (dm <= 1) continue;
-                    uint32_t b0, b1;
-                    vrange(a, j, B, l, b0, b1);
-                    if (b1 == b0) continue;
-                    const TabEntry te = te0[dm - 2];
-                    if (te.pbar == 0.0) continue;
-                    type2_event<D>(a, A, B, l, i, j, te, a0, nA, b0, b1 - b0, c);
-                }
-            } else {
-                int off[D], lo_[D];
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    lo_[k] = -2 - (int)(ac[k] & 1u);
-                    off[k] = lo_[k];
-                }
-                while (true) {
-                    int dm = 0;
-#pragma unroll
-                    for (int k = 0; k < D; ++k) dm = max(dm, abs(off[k]));
-                    if (dm >= 2) {
-                        uint32_t bc[D];
-#pragma unroll
-                        for (int k = 0; k < D; ++k) bc[k] = (ac[k] + (uint32_t)off[k]) & mask;
-                        const uint32_t B = morton_encode<D>(bc);
-                        if (!(i == j && B <= A)) {
-                            uint32_t b0, b1;
-                            vrange(a, j, B, l, b0, b1);
-                            if (b1 > b0) {
-                                const TabEntry te = te0[dm - 2];
-                                if (te.pbar != 0.0) type2_event<D>(a, A, B, l, i, j, te, a0, nA, b0, b1 - b0, c);
-                            }
-                        }
-                    }
-                    int k = 0;
-                    while (k < D && off[k] == lo_[k] + 5) { off[k] = lo_[k]; ++k; }
-                    if (k == D) break;
-                    ++off[k];
-                }
-            }
-        }
-    }
-    if (a.stats) {
-        atomicAdd(&a.stats->cand1, c.cand1);
-        atomicAdd(&a.stats->ev2, c.ev2);
-        atomicAdd(&a.stats->chunks, c.chunks);
-        atomicAdd(&a.stats->draws, c.draws);
-        atomicAdd(&a.stats->landings, c.landings);
-        atomicAdd(&a.stats->edges1, c.edges1);
-        atomicAdd(&a.stats->edges2, c.edges2);
-        atomicAdd(&a.stats->nt1, c.nt1);
-        atomicAdd(&a.stats->nt2, c.nt2);
-    }
-}
+// K5: sampling kernels
+#include "sample.cuh"
 
 // ======================================================================================
 // Host side
@@ -766,6 +478,7 @@ static double exact_W(const std::vector<WPartial>& parts, int emin)
 struct HostPlan {
     Plan p;
     std::vector<TabEntry> tab;
+    std::vector<uint16_t> tasks;
     uint64_t K = 0;
     double W = 0;
 };
@@ -851,6 +564,34 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
             }
     }
     if (hp.tab.empty()) hp.tab.push_back(TabEntry{0, 0, 0, 0});
+    // task lists: a point of layer i that is first in its cell from level lf on owns, for every
+    // nonempty partner j >= i with CL(i,j) >= lf, the type-I events at CL(i,j) and the type-II
+    // events at levels max(lf,2)..CL(i,j)
+    hp.tasks.clear();
+    for (int k = 0; k < 2; ++k)
+        for (int i = 0; i < p.L; ++i)
+            for (int lf = 0; lf < 32; ++lf) {
+                p.toff[k][i * 32 + lf] = (uint32_t)hp.tasks.size();
+                uint32_t c = 0;
+                if (p.cnt[i] && lf <= p.I[i])
+                    for (int j = i; j < p.L; ++j) {
+                        if (!p.cnt[j]) continue;
+                        const int cl = p.CL[i * MAXL + j];
+                        if (lf > cl) continue;
+                        if (k == 0) {
+                            hp.tasks.push_back((uint16_t)(j | (cl << 6)));
+                            ++c;
+                        } else if (T > 0.0) {
+                            for (int l = std::max(lf, 2); l <= cl; ++l) {
+                                hp.tasks.push_back((uint16_t)(j | (l << 6)));
+                                ++c;
+                            }
+                        }
+                    }
+                if (c > 0xFFFF) return GIRG_ERANGE;
+                p.tcnt[k][i * 32 + lf] = (uint16_t)c;
+            }
+    if (hp.tasks.empty()) hp.tasks.push_back(0);
     return GIRG_OK;
 }
 
@@ -899,11 +640,38 @@ static void launch_index(const double* w, const double* x, uint32_t n, const Pla
     GCHECK(cudaGetLastError());
 }
 
+template <int D, bool STATS>
+static void launch_sample_t(const SampleArgs& a, cudaStream_t st)
+{
+    int dev = 0, nsm = 148, occ = 1, occ2 = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sample<D, STATS>, SB, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_big<D, STATS>, SB, 0);
+    unsigned grid = std::max(1u, std::min<unsigned>(a.ntiles, (unsigned)(nsm * std::max(occ, 1))));
+    if (const char* g = getenv("GIRG_SAMPLE_GRID")) grid = std::max(1u, std::min<unsigned>(a.ntiles, (unsigned)atoi(g)));
+    static const bool sync_debug = getenv("GIRG_SYNC_DEBUG") != nullptr;
+    k_sample<D, STATS><<<grid, SB, 0, st>>>(a);
+    GCHECK(cudaGetLastError());
+    if (sync_debug) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        fprintf(stderr, "[girg] k_sample<%d,%d> grid %u: %s\n", D, (int)STATS, grid, cudaGetErrorString(e));
+        GCHECK(e);
+    }
+    k_big<D, STATS><<<(unsigned)(nsm * std::max(occ2, 1)), SB, 0, st>>>(a);
+    GCHECK(cudaGetLastError());
+    if (sync_debug) {
+        cudaError_t e = cudaStreamSynchronize(st);
+        fprintf(stderr, "[girg] k_big<%d,%d>: %s\n", D, (int)STATS, cudaGetErrorString(e));
+        GCHECK(e);
+    }
+}
+
 template <int D>
 static void launch_sample(const SampleArgs& a, cudaStream_t st)
 {
-    k_sample<D><<<grid_for(a.n, 256), 256, 0, st>>>(a);
-    GCHECK(cudaGetLastError());
+    if (a.stats) launch_sample_t<D, true>(a, st);
+    else launch_sample_t<D, false>(a, st);
 }
 
 static int edges_impl(const double* w, const double* x, uint64_t n, int d, double T, double kappa,
@@ -935,6 +703,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         // scratch
         Plan* d_plan = S.alloc<Plan>(1);
         TabEntry* d_tab = S.alloc<TabEntry>(hp.tab.size());
+        uint16_t* d_tasks = S.alloc<uint16_t>(hp.tasks.size());
         char* misc = S.alloc<char>(256);
         int* d_err = (int*)misc;
         unsigned long long* d_m = (unsigned long long*)(misc + 16);
@@ -950,6 +719,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         double* sx = S.alloc<double>((size_t)d * n);
         GCHECK(cudaMemcpyAsync(d_plan, &hp.p, sizeof(Plan), cudaMemcpyHostToDevice, st));
         GCHECK(cudaMemcpyAsync(d_tab, hp.tab.data(), hp.tab.size() * sizeof(TabEntry), cudaMemcpyHostToDevice, st));
+        GCHECK(cudaMemcpyAsync(d_tasks, hp.tasks.data(), hp.tasks.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
         GCHECK(cudaMemsetAsync(misc, 0, 256, st));
         PE.record(1, st);
         switch (d) {
@@ -962,36 +732,59 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         SampleArgs a;
         a.pl = d_plan;
         a.tab = d_tab;
+        a.tasks = d_tasks;
         a.skey = skey;
         a.sx = sx;
         a.sw = sw;
         a.sid = sid;
         a.P = P;
         a.n = n32;
+        a.ntiles = (n32 + SB - 1) / SB;
         a.k0 = (uint32_t)seed;
         a.k1 = (uint32_t)(seed >> 32);
         a.edges = (uint2*)edges;
         a.cap = cap;
         a.m = d_m;
+        a.tile_ctr = (unsigned int*)(misc + 24);
+        a.nitems = (unsigned int*)(misc + 28);
         a.stats = stats_out ? d_cnt : nullptr;
         a.err = d_err;
+        unsigned int items_cap = std::max<unsigned int>(1u << 16, n32 / 8);
+        a.items = S.alloc<BigItem>(items_cap);
+        a.items_cap = items_cap;
+        a.nP = K + 1;
+        a.ntab = (unsigned)hp.tab.size();
+        a.ntasks = (unsigned)hp.tasks.size();
         PE.record(2, st);
-        switch (d) {
-            case 1: launch_sample<1>(a, st); break;
-            case 2: launch_sample<2>(a, st); break;
-            case 3: launch_sample<3>(a, st); break;
-            case 4: launch_sample<4>(a, st); break;
-            default: launch_sample<5>(a, st); break;
-        }
-        PE.record(3, st);
         char hmisc[256];
-        GCHECK(cudaMemcpyAsync(hmisc, misc, 256, cudaMemcpyDeviceToHost, st));
-        GCHECK(cudaStreamSynchronize(st));
+        for (int attempt = 0;; ++attempt) {
+            switch (d) {
+                case 1: launch_sample<1>(a, st); break;
+                case 2: launch_sample<2>(a, st); break;
+                case 3: launch_sample<3>(a, st); break;
+                case 4: launch_sample<4>(a, st); break;
+                default: launch_sample<5>(a, st); break;
+            }
+            PE.record(3, st);
+            GCHECK(cudaMemcpyAsync(hmisc, misc, 256, cudaMemcpyDeviceToHost, st));
+            GCHECK(cudaStreamSynchronize(st));
+            int e0;
+            unsigned int need;
+            std::memcpy(&e0, hmisc, sizeof(int));
+            std::memcpy(&need, hmisc + 28, sizeof(need));
+            if (!(e0 & ERR_ITEMS) || attempt > 4) break;
+            // the big-event item queue overflowed: grow it and re-run the (deterministic) sampler
+            items_cap = need + (need >> 2) + 1024;
+            a.items = S.alloc<BigItem>(items_cap);
+            a.items_cap = items_cap;
+            GCHECK(cudaMemsetAsync(misc, 0, 256, st));
+            PE.record(2, st);
+        }
         g_timings.ms_wstats = PE.ms(0, 1);
         g_timings.ms_index = PE.ms(1, 2);
         g_timings.ms_sample = PE.ms(2, 3);
         g_timings.ms_total = PE.ms(0, 3);
-        g_timings.launches = 8;  // k_wstats, k_keys, 3 x scan, k_scatter, k_gather, k_sample
+        g_timings.launches = 9;  // k_wstats, k_keys, 3 x scan, k_scatter, k_gather, k_sample, k_big
         g_timings.n = n;
         g_timings.key_space = K;
         g_timings.d = d;
@@ -1003,7 +796,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         std::memcpy(&hc, hmisc + 32, sizeof(hc));
         g_timings.m = m;
         if (derr & ERR_POS) return GIRG_EINVAL;
-        if (derr & ERR_CHUNKS) return GIRG_ERANGE;
+        if (derr & ERR_ITEMS) return GIRG_ENOMEM;
         *m_out = m;
         if (stats_out) {
             stats_out->cand1 = hc.cand1;
