@@ -120,6 +120,29 @@ int girg_edges_shard(const double *w_dev, const double *x_dev, uint64_t n, int d
                      uint64_t blk_hi, uint32_t *edges_dev, uint64_t cap, uint64_t *m_out,
                      girg_stats *stats_out, void *stream);
 
+/* type-II sampling schemes (R10 / R22).  Both give exactly the GIRG distribution;
+ * for a fixed seed they give different (each deterministic) edge sets. */
+#define GIRG_SCHEME_EVENT 0  /* one geometric-jump sequence per distant cell pair: Alg. 1 lines 5-6
+                                as written, chunks of 2..4 expected landings */
+#define GIRG_SCHEME_MERGED 1 /* default: the distant cells of an A cell with the same bound class
+                                concatenated into one sequence (memorylessness of the jumps,
+                                P:494-501), chunks of 8..16 expected landings */
+
+typedef struct {
+    int scheme;           /* GIRG_SCHEME_MERGED (default) or GIRG_SCHEME_EVENT */
+    int shard_level;      /* as girg_edges_shard; 0, [0, 1) = the whole graph */
+    uint64_t blk_lo, blk_hi;
+} girg_options;
+
+/*
+ * girg_edges_ex -- girg_edges with explicit options (NULL = defaults: merged scheme, whole
+ * graph) and optional work counters (stats_out may be NULL).  Same semantics and errors as
+ * girg_edges_shard, plus EINVAL for an unknown scheme.
+ */
+int girg_edges_ex(const double *w_dev, const double *x_dev, uint64_t n, int d, double T,
+                  double kappa, uint64_t seed, const girg_options *opt, uint32_t *edges_dev,
+                  uint64_t cap, uint64_t *m_out, girg_stats *stats_out, void *stream);
+
 /*
  * girg_edges_host -- end-to-end variant with HOST buffers: copies w_host[n] and x_host[d*n]
  * to the device, runs girg_edges and copies the edges back into edges_host[cap][2].

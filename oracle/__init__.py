@@ -20,6 +20,7 @@ _SRC = os.path.join(_HERE, "girg_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 OK, EINVAL, ECAPACITY, ERANGE, ENOMEM = 0, -1, -2, -3, -4
+SCHEME_EVENT, SCHEME_MERGED = 0, 1  # type-II: per cell pair (Alg. 1 as written) / merged (R22)
 
 
 def build(force: bool = False) -> str:
@@ -78,7 +79,7 @@ def lib():
         L.or_are_neighbors.argtypes = [C.c_uint32, C.c_uint32, i32, i32]; L.or_are_neighbors.restype = i32
         L.or_delta_max.argtypes = [C.c_uint32, C.c_uint32, i32, i32]; L.or_delta_max.restype = i32
         L.or_levels.argtypes = [dp, u64, i32, d, C.POINTER(Levels)]; L.or_levels.restype = i32
-        L.or_edges.argtypes = [dp, dp, u64, i32, d, d, u64, i32, u64, u64, u32p, u64,
+        L.or_edges.argtypes = [dp, dp, u64, i32, d, d, u64, i32, u64, u64, i32, u32p, u64,
                                C.POINTER(C.c_uint64), C.POINTER(Stats)]
         L.or_edges.restype = i32
         L.or_bruteforce_t0.argtypes = [dp, dp, u64, i32, d, u32p, u64, C.POINTER(C.c_uint64)]
@@ -91,7 +92,7 @@ def lib():
         L.or_scale_weights.argtypes = [dp, u64, d, i32, d, d, dp]; L.or_scale_weights.restype = i32
         L.or_geometric_skip.argtypes = [d, d]; L.or_geometric_skip.restype = C.c_int64
         u64p = C.POINTER(C.c_uint64)
-        L.or_coverage.argtypes = [dp, dp, u64, i32, d, d, u32p, C.POINTER(Stats)]; L.or_coverage.restype = i32
+        L.or_coverage.argtypes = [dp, dp, u64, i32, d, d, i32, u32p, C.POINTER(Stats)]; L.or_coverage.restype = i32
         L.or_index.argtypes = [dp, dp, u64, i32, d, u32p, u64p, u32p, u64p, u64]; L.or_index.restype = i32
         L.or_count_pairs.argtypes = [i32, i32, u64p, u64p, u64p, u64p]; L.or_count_pairs.restype = i32
     return _lib
@@ -206,9 +207,10 @@ def levels(w: np.ndarray, d: int, kappa: float) -> dict:
     }
 
 
-def edges(w, x, d, T, kappa, seed, shard=(0, 0, 1), cap=None, with_stats=False):
+def edges(w, x, d, T, kappa, seed, shard=(0, 0, 1), cap=None, with_stats=False, scheme=SCHEME_MERGED):
     """Run the oracle sampler.  Returns a (m, 2) uint32 array of (u<v) pairs, unsorted
-    (and the work counters when with_stats)."""
+    (and the work counters when with_stats).  scheme: SCHEME_MERGED (R22, default) or
+    SCHEME_EVENT (one type-II sequence per distant cell pair, Alg. 1 as written)."""
     w = np.ascontiguousarray(w, dtype=np.float64)
     x = np.ascontiguousarray(x, dtype=np.float64).reshape(d, -1)
     n = w.size
@@ -219,7 +221,7 @@ def edges(w, x, d, T, kappa, seed, shard=(0, 0, 1), cap=None, with_stats=False):
         m = C.c_uint64(0)
         st = Stats()
         rc = lib().or_edges(_dp(w), _dp(x), n, d, float(T), float(kappa), C.c_uint64(seed),
-                            shard[0], C.c_uint64(shard[1]), C.c_uint64(shard[2]), _u32p(out),
+                            shard[0], C.c_uint64(shard[1]), C.c_uint64(shard[2]), scheme, _u32p(out),
                             cap, C.byref(m), C.byref(st))
         if rc == ECAPACITY:
             cap = int(m.value) + 1
@@ -289,14 +291,14 @@ def sort_edges(e: np.ndarray) -> np.ndarray:
     return np.sort(k)
 
 
-def coverage(w, x, d, T, kappa):
+def coverage(w, x, d, T, kappa, scheme=SCHEME_MERGED):
     """Instrumented oracle: (n, n) matrix of how often each ordered candidate (u, v) occurs."""
     w = np.ascontiguousarray(w, dtype=np.float64)
     x = np.ascontiguousarray(x, dtype=np.float64).reshape(d, -1)
     n = w.size
     cov = np.zeros((n, n), dtype=np.uint32)
     st = Stats()
-    rc = lib().or_coverage(_dp(w), _dp(x), n, d, float(T), float(kappa), _u32p(cov), C.byref(st))
+    rc = lib().or_coverage(_dp(w), _dp(x), n, d, float(T), float(kappa), scheme, _u32p(cov), C.byref(st))
     if rc:
         raise OracleError(rc)
     return cov, st.as_dict()

@@ -322,6 +322,9 @@ typedef struct {
     /* shard filter */
     int sl;
     uint64_t blo, bhi;
+    /* type-II scheme: OR_SCHEME_EVENT (one jump sequence per distant cell pair, Alg. 1 as
+     * written) or OR_SCHEME_MERGED (one sequence per (A cell, bound class), R22) */
+    int scheme;
     /* output */
     uint32_t *edges;
     uint64_t cap, m;
@@ -478,6 +481,136 @@ static void type2(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
     }
 }
 
+/* ---- R22: merged type-II sequences ----
+ * Alg. 1 samples every distant cell pair (A,B) of a bucket pair (i,j) on level l with its own
+ * geometric-jump sequence under the bound pbar(i,j,l,delta_max).  All distant
+ * pairs that share A and the bound class delta_max = k have the SAME pbar, so their candidate
+ * sets can be concatenated and jumped over as one sequence: each candidate is still landed on
+ * independently with probability pbar (memorylessness of the geometric skips), so
+ * the edge distribution is unchanged, while the per-pair terminating draws disappear.
+ *   D_k(A) = { B on level l : B and A not neighbours, parent(B) and parent(A) neighbours
+ *             (the distant pairs of Alg. 1), delta_max(A,B) = k, and B > A if i = j
+ *             (R16) }, in increasing Morton order.
+ *   candidates: row-major over V_i^A x (V_j^B for B in D_k(A), concatenated in that order).
+ *   chunks: C = 2^max(0, 3 - ilogb(pbar)) candidates (8..16 expected landings), doubled until
+ *   the sequence has < 2^32 chunks.  Draw r of chunk ch: Philox counter
+ *   (A, ch, l | i<<5 | j<<11 | (k-2)<<17 | 1<<18, r); r_jump = (o0,o1), r_acc = (o2,o3).
+ * Everything else (jump, stop test, acceptance r_acc*pbar < p_uv, near-tie log) is type2's. */
+static int cmp_u32(const void *a, const void *b)
+{
+    uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
+    return x < y ? -1 : x > y;
+}
+
+/* D_k(A) for both classes: out2/out3 receive the sorted cell lists, returns via n2/n3 */
+static void distant_cells(const or_ctx *c, int l, uint32_t A, int i, int j, uint32_t *out2,
+                          int *n2, uint32_t *out3, int *n3)
+{
+    int d = c->d;
+    uint32_t pa[5], q[5];
+    or_morton_decode(A >> d, d, l - 1, pa);
+    uint32_t side = 1u << (l - 1);
+    int noff = 1;
+    for (int k = 0; k < d; k++) noff *= 3;
+    *n2 = 0;
+    *n3 = 0;
+    for (int o = 0; o < noff; o++) { /* parent neighbours (torus), offsets in {-1,0,1}^d */
+        int r = o;
+        for (int k = 0; k < d; k++) {
+            int off = r % 3 - 1;
+            r /= 3;
+            q[k] = (pa[k] + side + (uint32_t)off) % side;
+        }
+        uint32_t P = or_morton_encode(q, d, l - 1);
+        for (uint32_t ch = 0; ch < (1u << d); ch++) {
+            uint32_t B = (P << d) | ch;
+            if (or_are_neighbors(A, B, d, l)) continue;
+            if (i == j && B <= A) continue;
+            int dm = or_delta_max(A, B, d, l);
+            uint32_t *out = dm == 2 ? out2 : out3;
+            int *no = dm == 2 ? n2 : n3;
+            int dup = 0; /* on levels <= 2 several offsets wrap onto the same parent */
+            for (int t = 0; t < *no; t++)
+                if (out[t] == B) { dup = 1; break; }
+            if (!dup) out[(*no)++] = B;
+        }
+    }
+    qsort(out2, (size_t)*n2, sizeof(uint32_t), cmp_u32);
+    qsort(out3, (size_t)*n3, sizeof(uint32_t), cmp_u32);
+}
+
+static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, const uint32_t *Bs, int nBs)
+{
+    uint64_t a0, a1;
+    vrange(c, i, A, l, &a0, &a1);
+    uint64_t nA = a1 - a0;
+    /* prefix of |V_j^B| over the concatenation */
+    uint64_t *pre = (uint64_t *)malloc(sizeof(uint64_t) * ((size_t)nBs + 1));
+    uint64_t *b0 = (uint64_t *)malloc(sizeof(uint64_t) * ((size_t)nBs + 1));
+    pre[0] = 0;
+    for (int t = 0; t < nBs; t++) {
+        uint64_t lo, hi;
+        vrange(c, j, Bs[t], l, &lo, &hi);
+        b0[t] = lo;
+        pre[t + 1] = pre[t] + (hi - lo);
+    }
+    uint64_t M = pre[nBs], N = nA * M;
+    if (N == 0) { free(pre); free(b0); return; }
+    c->st->ev2_nonempty++;
+    c->st->cand2 += N;
+    const uint32_t *Va = c->order + c->lstart[i], *Vb = c->order + c->lstart[j];
+    if (c->cover) {
+        for (uint64_t s = a0; s < a1; s++)
+            for (int t = 0; t < nBs; t++)
+                for (uint64_t v = b0[t]; v < b0[t] + (pre[t + 1] - pre[t]); v++)
+                    c->cover[(uint64_t)Va[s] * c->n + Vb[v]]++;
+        free(pre); free(b0);
+        return;
+    }
+    size_t ti = TAB(c, i, j, l, k - 2);
+    double pbar = c->pbar[ti], Lbar = c->Lbar[ti];
+    if (pbar == 0.0) { free(pre); free(b0); return; }
+    int cl2 = 0;
+    cl2 = 3 - ilogb(pbar);
+    if (cl2 < 0) cl2 = 0;
+    if (cl2 > 62) cl2 = 62;
+    while (((N - 1) >> cl2) >= (1ull << 32)) cl2++;
+    uint64_t C = 1ull << cl2;
+    uint64_t nch = (N - 1) / C + 1;
+    uint32_t tag = (uint32_t)l | ((uint32_t)i << 5) | ((uint32_t)j << 11) | ((uint32_t)(k - 2) << 17) | (1u << 18);
+    double xu[5], xv[5];
+    for (uint64_t ch = 0; ch < nch; ch++) {
+        c->st->chunks++;
+        uint64_t start = ch * C, end = start + C < N ? start + C : N;
+        int64_t pos = (int64_t)start - 1;
+        for (uint32_t r = 0;; r++) {
+            uint32_t ctr[4] = {A, (uint32_t)ch, tag, r}, o[4];
+            or_philox4x32_10(ctr, c->seed, o);
+            c->st->draws++;
+            double rj = or_u53(o[0], o[1]), ra = or_u53(o[2], o[3]);
+            double z = pbar == 1.0 ? 0.0 : log(1.0 - rj) / Lbar;
+            int64_t remaining = (int64_t)end - pos - 1;
+            if (z < (double)remaining + 1.0 && pbar < 1.0) { /* jump near-tie, as in type2 */
+                double az = fabs(z);
+                if (fabs(z - nearbyint(z)) < 1e-14 * (az > 1.0 ? az : 1.0)) c->st->nt2jump++;
+            }
+            if (z >= (double)remaining) break;
+            pos += 1 + (int64_t)z;
+            c->st->landings++;
+            uint64_t sidx = (uint64_t)pos / M, tidx = (uint64_t)pos % M;
+            int t = 0;
+            while (pre[t + 1] <= tidx) t++; /* the B cell holding concatenated index tidx */
+            uint32_t u = Va[a0 + sidx], v = Vb[b0[t] + (tidx - pre[t])];
+            double D = or_dpow(or_torus_dist(xcoord(c, u, xu), xcoord(c, v, xv), c->d), c->d);
+            double p = or_prob(c->w[u], c->w[v], c->s, D, c->T);
+            if (fabs(ra * pbar - p) < 1e-12 * pbar) c->st->nt2acc++;
+            if (ra * pbar < p) { c->st->acc2++; emit(c, u, v); }
+        }
+    }
+    free(pre);
+    free(b0);
+}
+
 /* shard ownership of an event whose A cell is at level l */
 static uint64_t blk_of(const or_ctx *c, int l, uint32_t A)
 {
@@ -518,13 +651,47 @@ static void recur(or_ctx *c, int l, uint32_t A, uint32_t B)
                 for (uint32_t y = 0; y < nc; y++)
                     recur(c, l + 1, (A << c->d) | x, (B << c->d) | y);
         }
-    } else if (c->T > 0.0 && own) {
+    } else if (c->T > 0.0 && own && c->scheme == OR_SCHEME_EVENT) {
         for (int k = 0; k < c->nge[l]; k++) {
             int i = c->ge[l][k][0], j = c->ge[l][k][1];
             if (i == j && A >= B) continue;
             type2(c, l, A, B, i, j);
         }
     }
+}
+
+/* R22 driver: for every level l >= 2, bucket pair (i,j) with CL(i,j) >= l, and
+ * nonempty A cell of bucket i on level l (visited in Morton order through the sorted index),
+ * the two merged sequences of classes delta_max = 2, 3. */
+static void merged_all(or_ctx *c)
+{
+    int d = c->d, noff = 1;
+    for (int k = 0; k < d; k++) noff *= 6;
+    uint32_t *l2 = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)noff);
+    uint32_t *l3 = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)noff);
+    for (int l = 2; l <= c->lv.maxCL; l++)
+        for (int pr = 0; pr < c->nge[l]; pr++) {
+            int i = c->ge[l][pr][0], j = c->ge[l][pr][1];
+            int sh = d * (c->lv.I[i] - l);
+            const uint32_t *Va = c->order + c->lstart[i];
+            uint64_t ni = c->lstart[i + 1] - c->lstart[i];
+            uint32_t prevA = 0;
+            for (uint64_t s = 0; s < ni; s++) {
+                double xv[5];
+                uint32_t A = or_cell_of_point(xcoord(c, Va[s], xv), d, c->lv.I[i]) >> sh;
+                if (s > 0 && A == prevA) continue;
+                prevA = A;
+                uint64_t b = blk_of(c, l, A);
+                if (b < c->blo || b >= c->bhi) continue;
+                int n2, n3;
+                distant_cells(c, l, A, i, j, l2, &n2, l3, &n3);
+                c->st->ev2 += (uint64_t)(n2 + n3);
+                type2_merged(c, l, A, i, j, 2, l2, n2);
+                type2_merged(c, l, A, i, j, 3, l3, n3);
+            }
+        }
+    free(l2);
+    free(l3);
 }
 
 /* test hook output of the Lemma-1 index */
@@ -544,7 +711,7 @@ static uint64_t now_ns(void)
 }
 
 static int or_run(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
-                  uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi,
+                  uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi, int scheme,
                   uint32_t *edges, uint64_t cap, uint64_t *m_out, or_stats_t *st,
                   uint32_t *cover, or_index_out *ix)
 {
@@ -556,6 +723,7 @@ static int or_run(const double *w, const double *x, uint64_t n, int d, double T,
     if (!(T >= 0.0 && T < 1.0)) return OR_EINVAL;
     if (!(kappa > 0.0) || !isfinite(kappa)) return OR_EINVAL;
     if (shard_level < 0 || shard_level * d > 32 || blk_lo >= blk_hi) return OR_EINVAL;
+    if (scheme != OR_SCHEME_EVENT && scheme != OR_SCHEME_MERGED) return OR_EINVAL;
     for (uint64_t i = 0; i < (uint64_t)d * n; i++)
         if (!(x[i] >= 0.0 && x[i] < 1.0)) return OR_EINVAL;
 
@@ -567,7 +735,7 @@ static int or_run(const double *w, const double *x, uint64_t n, int d, double T,
     c->w = w; c->x = x; c->n = n; c->d = d; c->T = T; c->seed = seed;
     c->invT = T > 0.0 ? 1.0 / T : 0.0;
     c->s = c->lv.s;
-    c->sl = shard_level; c->blo = blk_lo; c->bhi = blk_hi;
+    c->sl = shard_level; c->blo = blk_lo; c->bhi = blk_hi; c->scheme = scheme;
     c->edges = edges; c->cap = cap; c->st = st; c->cover = cover;
     const int L = c->lv.L;
 
@@ -674,6 +842,7 @@ static int or_run(const double *w, const double *x, uint64_t n, int d, double T,
     }
     uint64_t t1 = now_ns();
     recur(c, 0, 0u, 0u);
+    if (c->T > 0.0 && c->scheme == OR_SCHEME_MERGED) merged_all(c);
     st->ns_pre = t1 - t0;
     st->ns_edges = now_ns() - t1;
     rc = c->err;
@@ -689,22 +858,22 @@ done:
 }
 
 int or_edges(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
-             uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi,
+             uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi, int scheme,
              uint32_t *edges, uint64_t cap, uint64_t *m_out, or_stats_t *st)
 {
-    return or_run(w, x, n, d, T, kappa, seed, shard_level, blk_lo, blk_hi, edges, cap, m_out, st,
-                  NULL, NULL);
+    return or_run(w, x, n, d, T, kappa, seed, shard_level, blk_lo, blk_hi, scheme, edges, cap,
+                  m_out, st, NULL, NULL);
 }
 
 /* instrumented oracle (SURVEY 8(c) "Coverage"): cover[u*n+v] += 1 for every candidate pair
  * (u in V_i^A, v in V_j^B) of every type-I and type-II event; T > 0 so both types occur. */
 int or_coverage(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
-                uint32_t *cover, or_stats_t *st)
+                int scheme, uint32_t *cover, or_stats_t *st)
 {
     uint64_t m = 0;
     if (!cover || n > 20000) return OR_EINVAL;
     memset(cover, 0, sizeof(uint32_t) * n * n);
-    return or_run(w, x, n, d, T, kappa, 0, 0, 0, 1, NULL, 0, &m, st, cover, NULL);
+    return or_run(w, x, n, d, T, kappa, 0, 0, 0, 1, scheme, NULL, 0, &m, st, cover, NULL);
 }
 
 int or_index(const double *w, const double *x, uint64_t n, int d, double kappa, uint32_t *order,
@@ -712,7 +881,7 @@ int or_index(const double *w, const double *x, uint64_t n, int d, double kappa, 
 {
     uint64_t m = 0;
     or_index_out ix = {order, lstart, P, poff, pcap};
-    return or_run(w, x, n, d, 0.0, kappa, 0, 0, 0, 1, NULL, 0, &m, NULL, NULL, &ix);
+    return or_run(w, x, n, d, 0.0, kappa, 0, 0, 0, 1, OR_SCHEME_EVENT, NULL, 0, &m, NULL, NULL, &ix);
 }
 
 /* Cell pairs enumerated by Algorithm 1 on a full tree of depth `depth`,

@@ -73,19 +73,25 @@ typedef struct {
     uint64_t ns_pre, ns_edges;     /* wall time: levels + index ("Pre"), recursion ("Edges") */
 } or_stats_t;
 
+/* type-II schemes: EVENT = one jump sequence per distant cell pair (Alg. 1 lines 5-6 as
+ * written, R10); MERGED = one sequence per (A cell, bound class), the distant pairs of A with
+ * the same bound concatenated (R22, exact in distribution; the product default). */
+#define OR_SCHEME_EVENT 0
+#define OR_SCHEME_MERGED 1
+
 /* Edge sampler: Algorithm 1 over the Lemma-1 index, double counting
- * per App. B.1 (R16), type-II by geometric jumps (R10).
+ * per App. B.1 (R16), type-II by geometric jumps (R10 / R22).
  * Shard filter: only events whose A cell's block at shard_level lies in
  * [blk_lo, blk_hi) are processed; shard_level=0, [0,1) = everything.
  * edges: [cap][2] uint32 (u<v).  Returns OR_OK / OR_ECAPACITY (m_out = true m) / errors. */
 int or_edges(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
-             uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi,
+             uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi, int scheme,
              uint32_t *edges, uint64_t cap, uint64_t *m_out, or_stats_t *st);
 
 /* test hooks: instrumented coverage (cover: n*n counters), Lemma-1 index export, and the
  * per-level cell-pair counts of Algorithm 1 on a full tree */
 int or_coverage(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
-                uint32_t *cover, or_stats_t *st);
+                int scheme, uint32_t *cover, or_stats_t *st);
 int or_index(const double *w, const double *x, uint64_t n, int d, double kappa, uint32_t *order,
              uint64_t *lstart, uint32_t *P, uint64_t *poff, uint64_t pcap);
 int or_count_pairs(int d, int depth, uint64_t *nb, uint64_t *ds, uint64_t *ds2, uint64_t *ds3);

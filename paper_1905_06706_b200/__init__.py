@@ -23,6 +23,7 @@ if os.environ.get("GIRG_LIBRARY"):  # e.g. the bounds-checked libgirg_debug.so
     _LIB_PATH = os.environ["GIRG_LIBRARY"]
 
 OK, EINVAL, ECAPACITY, ERANGE, ENOMEM, ECUDA = 0, -1, -2, -3, -4, -5
+SCHEME_EVENT, SCHEME_MERGED = 0, 1  # include/girg.h GIRG_SCHEME_*
 
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
@@ -38,6 +39,10 @@ class Stats(C.Structure):
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
+class Options(C.Structure):
+    _fields_ = [("scheme", C.c_int), ("shard_level", C.c_int), ("blk_lo", C.c_uint64), ("blk_hi", C.c_uint64)]
 
 
 class Timings(C.Structure):
@@ -56,17 +61,19 @@ _lib.girg_scale_weights.argtypes = [_vp, _u64, _d, _i, _d, _d, C.POINTER(_d), _v
 _lib.girg_edges.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, _vp, _u64, C.POINTER(_u64), _vp]
 _lib.girg_edges_shard.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, _i, _u64, _u64, _vp, _u64,
                                   C.POINTER(_u64), C.POINTER(Stats), _vp]
+_lib.girg_edges_ex.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, C.POINTER(Options), _vp, _u64,
+                               C.POINTER(_u64), C.POINTER(Stats), _vp]
 _lib.girg_edges_host.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, _vp, _u64, C.POINTER(_u64), _vp]
 _lib.girg_last_timings.argtypes = [C.POINTER(Timings)]
 _lib.girg_strerror.argtypes = [_i]
 _lib.girg_strerror.restype = C.c_char_p
 _lib.girg_last_cuda_error.restype = C.c_char_p
 for _f in ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
-           "girg_edges_host", "girg_version", "girg_last_timings"):
+           "girg_edges_ex", "girg_edges_host", "girg_version", "girg_last_timings"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTS = ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
-           "girg_edges_host", "girg_strerror", "girg_last_cuda_error", "girg_version", "girg_last_timings")
+           "girg_edges_ex", "girg_edges_host", "girg_strerror", "girg_last_cuda_error", "girg_version", "girg_last_timings")
 
 
 class GirgError(RuntimeError):
@@ -127,8 +134,9 @@ def scale_weights(w: torch.Tensor, avg_deg: float, d: int, T: float, beta: float
 
 
 def edges(w: torch.Tensor, x: torch.Tensor, T: float, kappa: float, seed: int, cap: int | None = None,
-          out: torch.Tensor | None = None, shard=(0, 0, 1), stats: bool = False, stream=None):
-    """Sample the edge list (include/girg.h girg_edges / girg_edges_shard).
+          out: torch.Tensor | None = None, shard=(0, 0, 1), stats: bool = False, stream=None,
+          scheme: int = SCHEME_MERGED):
+    """Sample the edge list (include/girg.h girg_edges_ex; scheme SCHEME_MERGED = girg_edges).
 
     Returns an int32 CUDA tensor [m, 2] holding the uint32 pairs (u < v) (and the work counters
     when ``stats``).  If ``cap`` (or ``out``) is too small the call is re-issued once with the
@@ -147,9 +155,9 @@ def edges(w: torch.Tensor, x: torch.Tensor, T: float, kappa: float, seed: int, c
         buf = out if out is not None else torch.empty((cap, 2), dtype=torch.int32, device=w.device)
         m = C.c_uint64(0)
         st = Stats()
-        rc = _lib.girg_edges_shard(w.data_ptr(), x.data_ptr(), n, d, T, kappa, seed, shard[0], shard[1], shard[2],
-                                   buf.data_ptr(), cap, C.byref(m), C.byref(st) if stats else None,
-                                   _stream(stream))
+        opt = Options(scheme, shard[0], shard[1], shard[2])
+        rc = _lib.girg_edges_ex(w.data_ptr(), x.data_ptr(), n, d, T, kappa, seed, C.byref(opt), buf.data_ptr(), cap,
+                                C.byref(m), C.byref(st) if stats else None, _stream(stream))
         if rc == ECAPACITY and out is None:
             cap = int(m.value)
             continue

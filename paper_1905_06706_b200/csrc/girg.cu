@@ -42,8 +42,8 @@ constexpr int ERR_WEIGHT = 1, ERR_WRANGE = 2, ERR_POS = 4;
 struct TabEntry {
     double pbar;  // type-II bound for (i, j, level, class)
     double Lbar;  // log1p(-pbar)
-    int clog2;    // chunk length C = 2^clog2 candidates
-    int pad;
+    int clog2;    // EVENT scheme: chunk length C = 2^clog2 candidates (2..4 expected landings, R10)
+    int clog2m;   // MERGED scheme: 2^clog2m candidates (8..16 expected landings, R22)
 };
 
 struct Plan {
@@ -57,10 +57,10 @@ struct Plan {
     uint8_t I[MAXL];
     uint8_t CL[MAXL * MAXL];
     uint32_t tab_off[MAXL * MAXL];
-    // enumeration task lists per (layer i, first level lf): entries j | l<<6
-    // in tasks[toff[k][i*32+lf] ...], tcnt[k][i*32+lf] entries; k = 0 type-I, 1 type-II
-    uint32_t toff[2][MAXL * 32];
-    uint16_t tcnt[2][MAXL * 32];
+    // task lists per (layer i, first level lf in 0..32): entries
+    // j | l<<6 | typeI<<12 | typeII<<13 in tasks[toff[i*33+lf] ...], tcnt[i*33+lf] entries
+    uint32_t toff[MAXL * 33];
+    uint16_t tcnt[MAXL * 33];
 };
 
 struct WPartial {
@@ -305,29 +305,33 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const uint32_t* __r
     }
 }
 
+// K5: sampling kernels (Geo<D> is also used by the index build below)
+#include "sample.cuh"
+
 // ======================================================================================
 // K3/K4: counting-sort placement; in-cell order by vertex id (R11) and payload gather
 // ======================================================================================
 __global__ void k_scatter(const uint32_t* __restrict__ key, uint32_t n, const uint32_t* __restrict__ P,
-                          uint32_t* __restrict__ cnt, uint32_t* __restrict__ tmp)
+                          uint32_t* __restrict__ cnt, uint32_t* __restrict__ tmp, uint32_t* __restrict__ tkey)
 {
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     const uint32_t k = key[v];
     const uint32_t slot = P[k] + atomicSub(&cnt[k], 1u) - 1u;
     tmp[slot] = v;
+    tkey[slot] = k;
 }
 
-template <int D>
-__global__ void k_gather(const uint32_t* __restrict__ tmp, const uint32_t* __restrict__ key, uint32_t n,
-                         const uint32_t* __restrict__ P, const double* __restrict__ w,
-                         const double* __restrict__ x, uint32_t* __restrict__ sid,
-                         uint32_t* __restrict__ skey, double* __restrict__ sw, double* __restrict__ sx)
+// in-cell order by vertex id (R11): the slot order of k_scatter is arbitrary inside a cell, the
+// rank of v among its cell's ids is its final position.  Writes the sorted id / key arrays and
+// the inverse permutation used by k_place.
+__global__ void k_order(const uint32_t* __restrict__ tmp, const uint32_t* __restrict__ tkey, uint32_t n,
+                        const uint32_t* __restrict__ P, uint32_t* __restrict__ sid, uint32_t* __restrict__ skey,
+                        uint32_t* __restrict__ inv)
 {
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const uint32_t v = tmp[s];
-    const uint32_t k = key[v];
+    const uint32_t v = tmp[s], k = tkey[s];
     const uint32_t lo = P[k], hi = P[k + 1];
     uint32_t pos = s;
     if (hi - lo > 1) {
@@ -337,13 +341,29 @@ __global__ void k_gather(const uint32_t* __restrict__ tmp, const uint32_t* __res
     }
     sid[pos] = v;
     skey[pos] = k;
-    sw[pos] = w[v];
-#pragma unroll
-    for (int c = 0; c < D; ++c) sx[(size_t)c * n + pos] = x[(size_t)c * n + v];
+    inv[v] = pos;
 }
 
-// K5: sampling kernels
-#include "sample.cuh"
+// sorted point records rec[pos] = (x_0, .., x_{d-1}, w): coalesced reads in vertex order,
+// one aligned 16/32/48-byte record write per vertex
+template <int D>
+__global__ void k_place(const uint32_t* __restrict__ inv, uint32_t n, const double* __restrict__ w,
+                        const double* __restrict__ x, double* __restrict__ rec)
+{
+    const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    constexpr int RW = Geo<D>::RECW;
+    double r[RW];
+#pragma unroll
+    for (int k = 0; k < RW; ++k) r[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) r[k] = x[(size_t)k * n + v];
+    r[D] = w[v];
+    double2* dst = reinterpret_cast<double2*>(rec + (size_t)inv[v] * RW);
+#pragma unroll
+    for (int k = 0; k < RW / 2; ++k) dst[k] = make_double2(r[2 * k], r[2 * k + 1]);
+}
+
 
 // ======================================================================================
 // Host side
@@ -555,42 +575,44 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
                         TabEntry e;
                         e.pbar = ratio >= 1.0 ? 1.0 : std::pow(ratio, p.invT);
                         e.Lbar = std::log1p(-e.pbar);
-                        int c2 = 0;
-                        if (e.pbar > 0.0) c2 = std::min(62, std::max(0, 1 - std::ilogb(e.pbar)));
+                        int c2 = 0, c2m = 0;
+                        if (e.pbar > 0.0) {
+                            c2 = std::min(62, std::max(0, 1 - std::ilogb(e.pbar)));   // R10
+                            c2m = std::min(62, std::max(0, 3 - std::ilogb(e.pbar)));  // R22
+                        }
                         e.clog2 = c2;
-                        e.pad = 0;
+                        e.clog2m = c2m;
                         hp.tab.push_back(e);
                     }
             }
     }
     if (hp.tab.empty()) hp.tab.push_back(TabEntry{0, 0, 0, 0});
-    // task lists: a point of layer i that is first in its cell from level lf on owns, for every
-    // nonempty partner j >= i with CL(i,j) >= lf, the type-I events at CL(i,j) and the type-II
-    // events at levels max(lf,2)..CL(i,j)
+    // task lists: a task (j, l) of layer i is a cell Cg of layer i on level
+    // lg = max(0, l - G) (G = Geo<D>::G) with its level-l descendants; it is owned by the first
+    // point of Cg: the one point of Cg whose first level lf (the coarsest level on which it is the
+    // first point of its cell; it stays first on every finer level) is <= lg.  Type-I if
+    // l == CL(i,j), type-II if 2 <= l (T > 0).
     hp.tasks.clear();
-    for (int k = 0; k < 2; ++k)
-        for (int i = 0; i < p.L; ++i)
-            for (int lf = 0; lf < 32; ++lf) {
-                p.toff[k][i * 32 + lf] = (uint32_t)hp.tasks.size();
-                uint32_t c = 0;
-                if (p.cnt[i] && lf <= p.I[i])
-                    for (int j = i; j < p.L; ++j) {
-                        if (!p.cnt[j]) continue;
-                        const int cl = p.CL[i * MAXL + j];
-                        if (lf > cl) continue;
-                        if (k == 0) {
-                            hp.tasks.push_back((uint16_t)(j | (cl << 6)));
-                            ++c;
-                        } else if (T > 0.0) {
-                            for (int l = std::max(lf, 2); l <= cl; ++l) {
-                                hp.tasks.push_back((uint16_t)(j | (l << 6)));
-                                ++c;
-                            }
-                        }
+    const int G = d == 1 ? 3 : 1;
+    for (int i = 0; i < p.L; ++i)
+        for (int lf = 0; lf <= 32; ++lf) {
+            p.toff[i * 33 + lf] = (uint32_t)hp.tasks.size();
+            uint32_t c = 0;
+            if (p.cnt[i] && lf <= p.I[i])
+                for (int j = i; j < p.L; ++j) {
+                    if (!p.cnt[j]) continue;
+                    const int cl = p.CL[i * MAXL + j];
+                    for (int l = 0; l <= cl; ++l) {
+                        const int lg = std::max(0, l - G);
+                        const int t1 = l == cl, t2 = T > 0.0 && l >= 2;
+                        if (lg < lf || (!t1 && !t2)) continue;
+                        hp.tasks.push_back((uint16_t)(j | (l << 6) | (t1 << 12) | (t2 << 13)));
+                        ++c;
                     }
-                if (c > 0xFFFF) return GIRG_ERANGE;
-                p.tcnt[k][i * 32 + lf] = (uint16_t)c;
-            }
+                }
+            if (c > 0xFFFF) return GIRG_ERANGE;
+            p.tcnt[i * 33 + lf] = (uint16_t)c;
+        }
     if (hp.tasks.empty()) hp.tasks.push_back(0);
     return GIRG_OK;
 }
@@ -625,8 +647,8 @@ static void run_wstats(const double* w, uint64_t n, cudaStream_t st, Scratch& S,
 
 template <int D>
 static void launch_index(const double* w, const double* x, uint32_t n, const Plan* d_plan, uint64_t K,
-                         uint32_t* key, uint32_t* cnt, uint32_t* P, uint32_t* bsum, uint32_t* tmp, uint32_t* sid,
-                         uint32_t* skey, double* sw, double* sx, int* d_err, cudaStream_t st)
+                         uint32_t* key, uint32_t* cnt, uint32_t* P, uint32_t* bsum, uint32_t* tmp, uint32_t* tkey,
+                         uint32_t* inv, uint32_t* sid, uint32_t* skey, double* rec, int* d_err, cudaStream_t st)
 {
     const uint64_t len = K + 1;
     GCHECK(cudaMemsetAsync(cnt, 0, len * sizeof(uint32_t), st));
@@ -635,49 +657,74 @@ static void launch_index(const double* w, const double* x, uint32_t n, const Pla
     k_scan_reduce<<<nb, SCAN_THREADS, 0, st>>>(cnt, len, bsum);
     k_scan_top<<<1, 1024, 0, st>>>(bsum, nb);
     k_scan_final<<<nb, SCAN_THREADS, 0, st>>>(cnt, len, bsum, P);
-    k_scatter<<<grid_for(n, 256), 256, 0, st>>>(key, n, P, cnt, tmp);
-    k_gather<D><<<grid_for(n, 256), 256, 0, st>>>(tmp, key, n, P, w, x, sid, skey, sw, sx);
+    k_scatter<<<grid_for(n, 256), 256, 0, st>>>(key, n, P, cnt, tmp, tkey);
+    k_order<<<grid_for(n, 256), 256, 0, st>>>(tmp, tkey, n, P, sid, skey, inv);
+    k_place<D><<<grid_for(n, 256), 256, 0, st>>>(inv, n, w, x, rec);
     GCHECK(cudaGetLastError());
 }
 
-template <int D, bool STATS>
+template <class K>
+static void smem_optin(K kern, size_t bytes)
+{
+    static thread_local std::vector<const void*> done;
+    const void* f = (const void*)kern;
+    for (const void* q : done)
+        if (q == f) return;
+    GCHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    GCHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    done.push_back(f);
+}
+
+template <int D, int SCHEME, bool STATS>
 static void launch_sample_t(const SampleArgs& a, cudaStream_t st)
 {
+    constexpr int WPB = Geo<D>::WPB, TPB = 32 * WPB;
+    const size_t smem = sizeof(WarpSmem<D>) * WPB;
+    smem_optin(k_sample<D, SCHEME, STATS>, smem);
+    smem_optin(k_big<D, SCHEME, STATS>, smem);
     int dev = 0, nsm = 148, occ = 1, occ2 = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sample<D, STATS>, SB, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_big<D, STATS>, SB, 0);
-    unsigned grid = std::max(1u, std::min<unsigned>(a.ntiles, (unsigned)(nsm * std::max(occ, 1))));
-    if (const char* g = getenv("GIRG_SAMPLE_GRID")) grid = std::max(1u, std::min<unsigned>(a.ntiles, (unsigned)atoi(g)));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sample<D, SCHEME, STATS>, TPB, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_big<D, SCHEME, STATS>, TPB, smem);
+    const unsigned wtiles = (a.ntiles + WPB - 1) / WPB;
+    unsigned grid = std::max(1u, std::min<unsigned>(wtiles, (unsigned)(nsm * std::max(occ, 1))));
+    if (const char* g = getenv("GIRG_SAMPLE_GRID")) grid = std::max(1u, std::min<unsigned>(wtiles, (unsigned)atoi(g)));
     static const bool sync_debug = getenv("GIRG_SYNC_DEBUG") != nullptr;
-    k_sample<D, STATS><<<grid, SB, 0, st>>>(a);
+    k_sample<D, SCHEME, STATS><<<grid, TPB, smem, st>>>(a);
     GCHECK(cudaGetLastError());
     if (sync_debug) {
         cudaError_t e = cudaStreamSynchronize(st);
-        fprintf(stderr, "[girg] k_sample<%d,%d> grid %u: %s\n", D, (int)STATS, grid, cudaGetErrorString(e));
+        fprintf(stderr, "[girg] k_sample<%d,%d,%d> grid %u smem %zu occ %d: %s\n", D, SCHEME, (int)STATS, grid, smem,
+                occ, cudaGetErrorString(e));
         GCHECK(e);
     }
-    k_big<D, STATS><<<(unsigned)(nsm * std::max(occ2, 1)), SB, 0, st>>>(a);
+    k_big<D, SCHEME, STATS><<<(unsigned)(nsm * std::max(occ2, 1)), TPB, smem, st>>>(a);
     GCHECK(cudaGetLastError());
     if (sync_debug) {
         cudaError_t e = cudaStreamSynchronize(st);
-        fprintf(stderr, "[girg] k_big<%d,%d>: %s\n", D, (int)STATS, cudaGetErrorString(e));
+        fprintf(stderr, "[girg] k_big<%d,%d,%d>: %s\n", D, SCHEME, (int)STATS, cudaGetErrorString(e));
         GCHECK(e);
     }
 }
 
 template <int D>
-static void launch_sample(const SampleArgs& a, cudaStream_t st)
+static void launch_sample(const SampleArgs& a, int scheme, cudaStream_t st)
 {
-    if (a.stats) launch_sample_t<D, true>(a, st);
-    else launch_sample_t<D, false>(a, st);
+    if (scheme == SCHEME_EVENT) {
+        if (a.stats) launch_sample_t<D, SCHEME_EVENT, true>(a, st);
+        else launch_sample_t<D, SCHEME_EVENT, false>(a, st);
+    } else {
+        if (a.stats) launch_sample_t<D, SCHEME_MERGED, true>(a, st);
+        else launch_sample_t<D, SCHEME_MERGED, false>(a, st);
+    }
 }
 
 static int edges_impl(const double* w, const double* x, uint64_t n, int d, double T, double kappa,
-                      uint64_t seed, int sl, uint64_t blo, uint64_t bhi, uint32_t* edges, uint64_t cap,
+                      uint64_t seed, int sl, uint64_t blo, uint64_t bhi, int scheme, uint32_t* edges, uint64_t cap,
                       uint64_t* m_out, girg_stats* stats_out, cudaStream_t st)
 {
+    if (scheme != SCHEME_EVENT && scheme != SCHEME_MERGED) return GIRG_EINVAL;
     if (!w || !x || !m_out || (cap && !edges)) return GIRG_EINVAL;
     if (n == 0 || n >= (1ull << 32) || d < 1 || d > 5) return GIRG_EINVAL;
     if (!(T >= 0.0 && T < 1.0) || !(kappa > 0.0) || !std::isfinite(kappa)) return GIRG_EINVAL;
@@ -710,36 +757,37 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         Counters* d_cnt = (Counters*)(misc + 32);
         uint32_t* key = S.alloc<uint32_t>(n);
         uint32_t* tmp = S.alloc<uint32_t>(n);
+        uint32_t* tkey = S.alloc<uint32_t>(n);
+        uint32_t* inv = S.alloc<uint32_t>(n);
         uint32_t* cnt = S.alloc<uint32_t>(K + 1);
         uint32_t* P = S.alloc<uint32_t>(K + 1);
         uint32_t* bsum = S.alloc<uint32_t>(grid_for(K + 1, SCAN_TILE) + 1);
         uint32_t* sid = S.alloc<uint32_t>(n);
         uint32_t* skey = S.alloc<uint32_t>(n);
-        double* sw = S.alloc<double>(n);
-        double* sx = S.alloc<double>((size_t)d * n);
+        const int recw = d == 1 ? 2 : (d <= 3 ? 4 : 6);
+        double* rec = S.alloc<double>((size_t)recw * n);
         GCHECK(cudaMemcpyAsync(d_plan, &hp.p, sizeof(Plan), cudaMemcpyHostToDevice, st));
         GCHECK(cudaMemcpyAsync(d_tab, hp.tab.data(), hp.tab.size() * sizeof(TabEntry), cudaMemcpyHostToDevice, st));
         GCHECK(cudaMemcpyAsync(d_tasks, hp.tasks.data(), hp.tasks.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
         GCHECK(cudaMemsetAsync(misc, 0, 256, st));
         PE.record(1, st);
         switch (d) {
-            case 1: launch_index<1>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, sid, skey, sw, sx, d_err, st); break;
-            case 2: launch_index<2>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, sid, skey, sw, sx, d_err, st); break;
-            case 3: launch_index<3>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, sid, skey, sw, sx, d_err, st); break;
-            case 4: launch_index<4>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, sid, skey, sw, sx, d_err, st); break;
-            default: launch_index<5>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, sid, skey, sw, sx, d_err, st); break;
+            case 1: launch_index<1>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
+            case 2: launch_index<2>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
+            case 3: launch_index<3>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
+            case 4: launch_index<4>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
+            default: launch_index<5>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
         }
         SampleArgs a;
         a.pl = d_plan;
         a.tab = d_tab;
         a.tasks = d_tasks;
         a.skey = skey;
-        a.sx = sx;
-        a.sw = sw;
+        a.rec = rec;
         a.sid = sid;
         a.P = P;
         a.n = n32;
-        a.ntiles = (n32 + SB - 1) / SB;
+        a.ntiles = (n32 + 31) / 32;
         a.k0 = (uint32_t)seed;
         a.k1 = (uint32_t)(seed >> 32);
         a.edges = (uint2*)edges;
@@ -749,7 +797,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         a.nitems = (unsigned int*)(misc + 28);
         a.stats = stats_out ? d_cnt : nullptr;
         a.err = d_err;
-        unsigned int items_cap = std::max<unsigned int>(1u << 16, n32 / 8);
+        unsigned int items_cap = std::max<unsigned int>(1u << 14, n32 / 64);
         a.items = S.alloc<BigItem>(items_cap);
         a.items_cap = items_cap;
         a.nP = K + 1;
@@ -759,11 +807,11 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         char hmisc[256];
         for (int attempt = 0;; ++attempt) {
             switch (d) {
-                case 1: launch_sample<1>(a, st); break;
-                case 2: launch_sample<2>(a, st); break;
-                case 3: launch_sample<3>(a, st); break;
-                case 4: launch_sample<4>(a, st); break;
-                default: launch_sample<5>(a, st); break;
+                case 1: launch_sample<1>(a, scheme, st); break;
+                case 2: launch_sample<2>(a, scheme, st); break;
+                case 3: launch_sample<3>(a, scheme, st); break;
+                case 4: launch_sample<4>(a, scheme, st); break;
+                default: launch_sample<5>(a, scheme, st); break;
             }
             PE.record(3, st);
             GCHECK(cudaMemcpyAsync(hmisc, misc, 256, cudaMemcpyDeviceToHost, st));
@@ -784,7 +832,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         g_timings.ms_index = PE.ms(1, 2);
         g_timings.ms_sample = PE.ms(2, 3);
         g_timings.ms_total = PE.ms(0, 3);
-        g_timings.launches = 9;  // k_wstats, k_keys, 3 x scan, k_scatter, k_gather, k_sample, k_big
+        g_timings.launches = 10;  // k_wstats, k_keys, 3 x scan, k_scatter, k_order, k_place, k_sample, k_big
         g_timings.n = n;
         g_timings.key_space = K;
         g_timings.d = d;
@@ -1076,7 +1124,7 @@ extern "C" int girg_scale_weights(const double* w_dev, uint64_t n, double avg_de
 extern "C" int girg_edges(const double* w_dev, const double* x_dev, uint64_t n, int d, double T, double kappa,
                           uint64_t seed, uint32_t* edges_dev, uint64_t cap, uint64_t* m_out, void* stream)
 {
-    return edges_impl(w_dev, x_dev, n, d, T, kappa, seed, 0, 0, 1, edges_dev, cap, m_out, nullptr,
+    return edges_impl(w_dev, x_dev, n, d, T, kappa, seed, 0, 0, 1, SCHEME_MERGED, edges_dev, cap, m_out, nullptr,
                       (cudaStream_t)stream);
 }
 
@@ -1085,8 +1133,18 @@ extern "C" int girg_edges_shard(const double* w_dev, const double* x_dev, uint64
                                 uint32_t* edges_dev, uint64_t cap, uint64_t* m_out, girg_stats* stats_out,
                                 void* stream)
 {
-    return edges_impl(w_dev, x_dev, n, d, T, kappa, seed, shard_level, blk_lo, blk_hi, edges_dev, cap, m_out,
-                      stats_out, (cudaStream_t)stream);
+    return edges_impl(w_dev, x_dev, n, d, T, kappa, seed, shard_level, blk_lo, blk_hi, SCHEME_MERGED, edges_dev,
+                      cap, m_out, stats_out, (cudaStream_t)stream);
+}
+
+extern "C" int girg_edges_ex(const double* w_dev, const double* x_dev, uint64_t n, int d, double T, double kappa,
+                             uint64_t seed, const girg_options* opt, uint32_t* edges_dev, uint64_t cap,
+                             uint64_t* m_out, girg_stats* stats_out, void* stream)
+{
+    girg_options o = {GIRG_SCHEME_MERGED, 0, 0, 1};
+    if (opt) o = *opt;
+    return edges_impl(w_dev, x_dev, n, d, T, kappa, seed, o.shard_level, o.blk_lo, o.blk_hi, o.scheme, edges_dev, cap,
+                      m_out, stats_out, (cudaStream_t)stream);
 }
 
 extern "C" int girg_edges_host(const double* w_host, const double* x_host, uint64_t n, int d, double T,
@@ -1103,7 +1161,7 @@ extern "C" int girg_edges_host(const double* w_host, const double* x_host, uint6
         uint32_t* e = S.alloc<uint32_t>(2 * std::max<uint64_t>(cap, 1));
         GCHECK(cudaMemcpyAsync(w, w_host, n * sizeof(double), cudaMemcpyHostToDevice, st));
         GCHECK(cudaMemcpyAsync(x, x_host, (size_t)d * n * sizeof(double), cudaMemcpyHostToDevice, st));
-        int rc = edges_impl(w, x, n, d, T, kappa, seed, 0, 0, 1, e, cap, m_out, nullptr, st);
+        int rc = edges_impl(w, x, n, d, T, kappa, seed, 0, 0, 1, SCHEME_MERGED, e, cap, m_out, nullptr, st);
         if (rc != GIRG_OK) return rc;
         if (*m_out) GCHECK(cudaMemcpyAsync(edges_host, e, *m_out * 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         GCHECK(cudaStreamSynchronize(st));
@@ -1137,4 +1195,4 @@ extern "C" int girg_last_timings(girg_timings* out)
 
 extern "C" const char* girg_last_cuda_error(void) { return girg::g_last_cuda.c_str(); }
 
-extern "C" int girg_version(void) { return 100; }
+extern "C" int girg_version(void) { return 200; }

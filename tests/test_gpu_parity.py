@@ -29,14 +29,14 @@ def gpu_keys(e):
     return girg.edge_keys(e).cpu().numpy().astype(np.uint64)
 
 
-def run_both(w, x, d, T, kappa, seed, shard=(0, 0, 1)):
-    e, st = girg.edges(dev(w), dev(x), T, kappa, seed, shard=shard, stats=True)
-    eo, so = O.edges(w, x, d, T, kappa, seed, shard=shard, with_stats=True)
+def run_both(w, x, d, T, kappa, seed, shard=(0, 0, 1), scheme=girg.SCHEME_MERGED):
+    e, st = girg.edges(dev(w), dev(x), T, kappa, seed, shard=shard, stats=True, scheme=scheme)
+    eo, so = O.edges(w, x, d, T, kappa, seed, shard=shard, with_stats=True, scheme=scheme)
     return gpu_keys(e), O.sort_edges(eo), st, so
 
 
-def assert_parity(w, x, d, T, kappa, seed, shard=(0, 0, 1)):
-    g, o, st, so = run_both(w, x, d, T, kappa, seed, shard)
+def assert_parity(w, x, d, T, kappa, seed, shard=(0, 0, 1), scheme=girg.SCHEME_MERGED):
+    g, o, st, so = run_both(w, x, d, T, kappa, seed, shard, scheme)
     assert so["nt1"] + so["nt2acc"] + so["nt2jump"] == 0, so
     assert len(g) == len(o), (len(g), len(o))
     assert np.array_equal(g, o)
@@ -96,24 +96,29 @@ def test_threshold_parity_all_dims(d):
 
 
 # ----------------------------------------------------------------- T > 0 -----------------
+SCHEMES = pytest.mark.parametrize("scheme", [girg.SCHEME_EVENT, girg.SCHEME_MERGED], ids=["event", "merged"])
+
+
+@SCHEMES
 @pytest.mark.parametrize("d,T,beta", [(1, 0.5, 2.5), (2, 0.8, 2.2), (3, 0.9, 2.9), (1, 0.2, 2.1),
                                       (2, 0.3, 3.0), (4, 0.6, 2.5), (5, 0.5, 2.7)])
-def test_binomial_parity_small(d, T, beta):
+def test_binomial_parity_small(d, T, beta, scheme):
     for n, seed in ((1, 1), (2, 2), (997, 3), (30_011, 4)):
         w, x = synth_inputs(n, d, beta, 7 * d + seed)
         kappa = O.scale_weights(w, min(10.0, max(n - 1.5, 0.5)), d, T, beta) if n > 2 else 0.7
-        g, st, so = assert_parity(w, x, d, T, kappa, seed)
+        g, st, so = assert_parity(w, x, d, T, kappa, seed, scheme=scheme)
         if n > 1000:
             assert so["landings"] > 0
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C3", "C4"])
-def test_baseline_config_full_parity(cfg):
+@pytest.mark.parametrize("cfg,scheme", [("C2", girg.SCHEME_MERGED), ("C3", girg.SCHEME_MERGED),
+                                        ("C4", girg.SCHEME_MERGED), ("C2", girg.SCHEME_EVENT)])
+def test_baseline_config_full_parity(cfg, scheme):
     """BASELINE configs 2-4 in full: identical edge sets, zero near-ties, degree on target."""
     c = BY_NAME[cfg]
     w, x = synth_inputs(c.n, c.d, c.beta, c.seed)
     kappa = O.scale_weights(w, c.avg_deg, c.d, c.T, c.beta)
-    g, st, so = assert_parity(w, x, c.d, c.T, kappa, c.seed)
+    g, st, so = assert_parity(w, x, c.d, c.T, kappa, c.seed, scheme=scheme)
     assert abs(2 * len(g) / c.n - c.avg_deg) < 0.01 * c.avg_deg
 
 

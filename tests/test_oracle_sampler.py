@@ -40,14 +40,19 @@ def test_threshold_C1_full_bruteforce(oracle):
     assert st["ev2"] == 0  # no type-II events at T = 0
 
 
+SCHEMES = pytest.mark.parametrize("scheme", [0, 1], ids=["event", "merged"])
+
+
+@SCHEMES
 @pytest.mark.parametrize("d,T", [(1, 0.5), (2, 0.8), (3, 0.9), (1, 0.2)])
-def test_coverage_each_pair_exactly_once(oracle, d, T):
+def test_coverage_each_pair_exactly_once(oracle, d, T, scheme):
     """every unordered vertex pair is a candidate of exactly one (cell pair, bucket pair)
-    event -- instrumented oracle on n <= 600."""
+    event -- instrumented oracle on n <= 600.  Merged sequences (R22) regroup the same events,
+    so the same exact cover must hold."""
     n = 600 if d < 3 else 400
     w, x = synth_inputs(n, d, 2.3, 77 + d)
     kappa = oracle.scale_weights(w, 4.0, d, T, 2.3)
-    cov, st = oracle.coverage(w, x, d, T, kappa)
+    cov, st = oracle.coverage(w, x, d, T, kappa, scheme=scheme)
     sym = cov.astype(np.int64) + cov.T.astype(np.int64)
     assert (np.diag(cov) == 0).all()
     off = ~np.eye(n, dtype=bool)
@@ -56,8 +61,9 @@ def test_coverage_each_pair_exactly_once(oracle, d, T):
     assert st["cand1"] + st["cand2"] == n * (n - 1) // 2
 
 
+@SCHEMES
 @pytest.mark.parametrize("d,T,runs", [(1, 0.5, 20000), (2, 0.8, 20000), (1, 0.3, 8000), (3, 0.9, 8000)])
-def test_per_pair_frequency(oracle, d, T, runs):
+def test_per_pair_frequency(oracle, d, T, runs, scheme):
     """with fixed w and x, each pair's empirical edge frequency over independent edge
     seeds is within 5 sigma of p_uv (Eq. 1), and the chi-square over pairs is plausible."""
     n = 40
@@ -73,7 +79,7 @@ def test_per_pair_frequency(oracle, d, T, runs):
     cnt = np.zeros((n, n))
     land = 0
     for seed in range(runs):
-        e, st = oracle.edges(w, x, d, T, kappa, seed + 1, with_stats=True)
+        e, st = oracle.edges(w, x, d, T, kappa, seed + 1, with_stats=True, scheme=scheme)
         land += st["landings"]
         cnt[e[:, 0], e[:, 1]] += 1
     assert land > 0  # type-II jumps were exercised
@@ -97,43 +103,62 @@ def test_per_pair_frequency(oracle, d, T, runs):
     assert abs(chi2 - k) < 6 * math.sqrt(2 * k), (chi2, k)
 
 
-def test_expected_edge_count(oracle):
+@SCHEMES
+def test_expected_edge_count(oracle, scheme):
     """mean of m over independent edge seeds vs sum_{u<v} p_uv (brute force), z < 4."""
     n, d, T = 3000, 2, 0.5
     w, x = synth_inputs(n, d, 2.5, 9)
     kappa = oracle.scale_weights(w, 8.0, d, T, 2.5)
     mu = oracle.expected_edges_bf(w, x, d, T, kappa)
-    ms = np.array([len(oracle.edges(w, x, d, T, kappa, s)) for s in range(1, 61)])
+    ms = np.array([len(oracle.edges(w, x, d, T, kappa, s, scheme=scheme)) for s in range(1, 61)])
     # var(m) = sum p(1-p) <= mu
     z = abs(ms.mean() - mu) / math.sqrt(mu / len(ms))
     assert z < 4, (ms.mean(), mu)
 
 
-def test_structure_and_determinism(oracle):
+@SCHEMES
+def test_structure_and_determinism(oracle, scheme):
     for d, T in ((1, 0.5), (2, 0.8), (3, 0.6)):
         n = 5000
         w, x = synth_inputs(n, d, 2.4, 31 + d)
         kappa = oracle.scale_weights(w, 10.0, d, T, 2.4)
-        e = oracle.edges(w, x, d, T, kappa, 7)
+        e = oracle.edges(w, x, d, T, kappa, 7, scheme=scheme)
         assert (e[:, 0] < e[:, 1]).all() and (e[:, 1] < n).all()
         k = keys(e)
         assert len(np.unique(k)) == len(k)
-        assert np.array_equal(k, keys(oracle.edges(w, x, d, T, kappa, 7)))
-        assert not np.array_equal(k, keys(oracle.edges(w, x, d, T, kappa, 8)))
+        assert np.array_equal(k, keys(oracle.edges(w, x, d, T, kappa, 7, scheme=scheme)))
+        assert not np.array_equal(k, keys(oracle.edges(w, x, d, T, kappa, 8, scheme=scheme)))
 
 
+def test_merged_scheme_reduces_draws(oracle):
+    """R22 does what it is for: same landings in expectation, far fewer Philox draws (the
+    per-cell-pair terminating draws disappear), and the same type-I work."""
+    n, d, T = 20000, 3, 0.9
+    w, x = synth_inputs(n, d, 2.9, 5)
+    kappa = oracle.scale_weights(w, 20.0, d, T, 2.9)
+    _, se = oracle.edges(w, x, d, T, kappa, 3, with_stats=True, scheme=0)
+    _, sm = oracle.edges(w, x, d, T, kappa, 3, with_stats=True, scheme=1)
+    assert se["cand1"] == sm["cand1"] and se["acc1"] == sm["acc1"]  # type-I keyed by (u, v)
+    assert se["cand2"] == sm["cand2"]  # the same candidate pairs, regrouped
+    assert sm["draws"] < 0.5 * se["draws"]
+    z = abs(sm["landings"] - se["landings"]) / math.sqrt(se["landings"] + sm["landings"])
+    assert z < 5, (se["landings"], sm["landings"])
+
+
+@SCHEMES
 @pytest.mark.parametrize("d", [1, 2, 3])
-def test_shards_partition_the_edge_set(oracle, d):
+def test_shards_partition_the_edge_set(oracle, d, scheme):
     """events are owned by the block of their A cell; shards are disjoint and
     their union is the full edge set (also exercised by the gloo multi-process test)."""
     n, T = 4000, 0.7
     w, x = synth_inputs(n, d, 2.3, 51 + d)
     kappa = oracle.scale_weights(w, 10.0, d, T, 2.3)
-    full = keys(oracle.edges(w, x, d, T, kappa, 3))
+    full = keys(oracle.edges(w, x, d, T, kappa, 3, scheme=scheme))
     for sl in (1, 2, 3):
         nb = 1 << (d * sl)
         cuts = sorted(set([0, nb // 3, nb // 2, nb]))
-        parts = [keys(oracle.edges(w, x, d, T, kappa, 3, shard=(sl, a, b))) for a, b in zip(cuts, cuts[1:])]
+        parts = [keys(oracle.edges(w, x, d, T, kappa, 3, shard=(sl, a, b), scheme=scheme))
+                 for a, b in zip(cuts, cuts[1:])]
         allp = np.concatenate(parts)
         assert len(allp) == len(full)
         assert np.array_equal(np.sort(allp), full)
@@ -149,7 +174,7 @@ def test_capacity_error_and_rerun(oracle):
     full = oracle.edges(w, x, d, T, kappa, 5)
     out = np.empty((10, 2), dtype=np.uint32)
     m = C.c_uint64(0)
-    rc = oracle.lib().or_edges(oracle._dp(w), oracle._dp(x), n, d, T, kappa, 5, 0, 0, 1,
+    rc = oracle.lib().or_edges(oracle._dp(w), oracle._dp(x), n, d, T, kappa, 5, 0, 0, 1, oracle.SCHEME_MERGED,
                                oracle._u32p(out), 10, C.byref(m), None)
     assert rc == oracle.ECAPACITY and int(m.value) == len(full)
     assert np.array_equal(keys(oracle.edges(w, x, d, T, kappa, 5, cap=len(full))), keys(full))
