@@ -50,6 +50,8 @@ typedef struct {
     uint64_t neartie2;   /* |r_acc - p_uv/pbar| < 1e-12 at a type-II acceptance  */
     uint64_t layers;     /* number of weight layers (buckets)                    */
     uint64_t key_space;  /* number of index cells sum_i 2^(d I(i))               */
+    uint64_t fast_fallback; /* decisions the float fast path left to the canonical double path */
+    uint64_t fast_mismatch; /* fast-path decisions that differ from the canonical one (must be 0) */
 } girg_stats;
 
 /*
@@ -126,7 +128,7 @@ int girg_edges_shard(const double *w_dev, const double *x_dev, uint64_t n, int d
                                 as written, chunks of 2..4 expected landings */
 #define GIRG_SCHEME_MERGED 1 /* default: the distant cells of an A cell with the same bound class
                                 concatenated into one sequence (memorylessness of the jumps,
-                                P:494-501), chunks of 8..16 expected landings */
+                                P:494-501), chunks of 2..4 expected landings */
 
 typedef struct {
     int scheme;           /* GIRG_SCHEME_MERGED (default) or GIRG_SCHEME_EVENT */

@@ -492,8 +492,8 @@ static void type2(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
  *             (the distant pairs of Alg. 1), delta_max(A,B) = k, and B > A if i = j
  *             (R16) }, in increasing Morton order.
  *   candidates: row-major over V_i^A x (V_j^B for B in D_k(A), concatenated in that order).
- *   chunks: C = 2^max(0, 3 - ilogb(pbar)) candidates (8..16 expected landings), doubled until
- *   the sequence has < 2^32 chunks.  Draw r of chunk ch: Philox counter
+ *   chunks: C = 2^max(0, 1 - ilogb(pbar)) candidates (2..4 expected landings, as R10), doubled
+ *   until the sequence has < 2^32 chunks.  Draw r of chunk ch: Philox counter
  *   (A, ch, l | i<<5 | j<<11 | (k-2)<<17 | 1<<18, r); r_jump = (o0,o1), r_acc = (o2,o3).
  * Everything else (jump, stop test, acceptance r_acc*pbar < p_uv, near-tie log) is type2's. */
 static int cmp_u32(const void *a, const void *b)
@@ -571,7 +571,7 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
     double pbar = c->pbar[ti], Lbar = c->Lbar[ti];
     if (pbar == 0.0) { free(pre); free(b0); return; }
     int cl2 = 0;
-    cl2 = 3 - ilogb(pbar);
+    cl2 = 1 - ilogb(pbar);
     if (cl2 < 0) cl2 = 0;
     if (cl2 > 62) cl2 = 62;
     while (((N - 1) >> cl2) >= (1ull << 32)) cl2++;

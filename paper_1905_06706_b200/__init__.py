@@ -35,7 +35,7 @@ _lib = C.CDLL(_LIB_PATH)
 class Stats(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in (
         "cand1", "ev2", "chunks", "draws", "landings", "edges1", "edges2",
-        "neartie1", "neartie2", "layers", "key_space")]
+        "neartie1", "neartie2", "layers", "key_space", "fast_fallback", "fast_mismatch")]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}

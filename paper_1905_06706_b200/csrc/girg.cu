@@ -43,7 +43,9 @@ struct TabEntry {
     double pbar;  // type-II bound for (i, j, level, class)
     double Lbar;  // log1p(-pbar)
     int clog2;    // EVENT scheme: chunk length C = 2^clog2 candidates (2..4 expected landings, R10)
-    int clog2m;   // MERGED scheme: 2^clog2m candidates (8..16 expected landings, R22)
+    int clog2m;   // MERGED scheme: 2^clog2m candidates (2..4 expected landings, R22)
+    double il2;   // 1 / log2(1 - pbar) = ln 2 / Lbar (fast jump path; unused when pbar = 1)
+    double pad;
 };
 
 struct Plan {
@@ -578,15 +580,17 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
                         int c2 = 0, c2m = 0;
                         if (e.pbar > 0.0) {
                             c2 = std::min(62, std::max(0, 1 - std::ilogb(e.pbar)));   // R10
-                            c2m = std::min(62, std::max(0, 3 - std::ilogb(e.pbar)));  // R22
+                            c2m = std::min(62, std::max(0, 1 - std::ilogb(e.pbar)));  // R22
                         }
                         e.clog2 = c2;
                         e.clog2m = c2m;
+                        e.il2 = e.pbar < 1.0 ? M_LN2 / e.Lbar : 0.0;
+                        e.pad = 0.0;
                         hp.tab.push_back(e);
                     }
             }
     }
-    if (hp.tab.empty()) hp.tab.push_back(TabEntry{0, 0, 0, 0});
+    if (hp.tab.empty()) hp.tab.push_back(TabEntry{0, 0, 0, 0, 0, 0});
     // task lists: a task (j, l) of layer i is a cell Cg of layer i on level
     // lg = max(0, l - G) (G = Geo<D>::G) with its level-l descendants; it is owned by the first
     // point of Cg: the one point of Cg whose first level lf (the coarsest level on which it is the
@@ -691,7 +695,15 @@ static void launch_sample_t(const SampleArgs& a, cudaStream_t st)
     unsigned grid = std::max(1u, std::min<unsigned>(wtiles, (unsigned)(nsm * std::max(occ, 1))));
     if (const char* g = getenv("GIRG_SAMPLE_GRID")) grid = std::max(1u, std::min<unsigned>(wtiles, (unsigned)atoi(g)));
     static const bool sync_debug = getenv("GIRG_SYNC_DEBUG") != nullptr;
-    k_sample<D, SCHEME, STATS><<<grid, TPB, smem, st>>>(a);
+    static const char* wprof_path = getenv("GIRG_WARP_PROFILE");  // development: per-warp profile dump
+    const unsigned gbig = (unsigned)(nsm * std::max(occ2, 1));
+    const size_t nwarps = (size_t)std::max(grid, gbig) * WPB;
+    SampleArgs b = a;
+    if (wprof_path) {
+        GCHECK(cudaMallocAsync(&b.wprof, 2 * nwarps * 4 * sizeof(unsigned long long), st));
+        GCHECK(cudaMemsetAsync(b.wprof, 0, 2 * nwarps * 4 * sizeof(unsigned long long), st));
+    }
+    k_sample<D, SCHEME, STATS><<<grid, TPB, smem, st>>>(b);
     GCHECK(cudaGetLastError());
     if (sync_debug) {
         cudaError_t e = cudaStreamSynchronize(st);
@@ -699,8 +711,22 @@ static void launch_sample_t(const SampleArgs& a, cudaStream_t st)
                 occ, cudaGetErrorString(e));
         GCHECK(e);
     }
-    k_big<D, SCHEME, STATS><<<(unsigned)(nsm * std::max(occ2, 1)), TPB, smem, st>>>(a);
+    if (b.wprof) b.wprof += nwarps * 4;
+    k_big<D, SCHEME, STATS><<<gbig, TPB, smem, st>>>(b);
     GCHECK(cudaGetLastError());
+    if (wprof_path) {
+        std::vector<unsigned long long> h(2 * nwarps * 4);
+        b.wprof -= nwarps * 4;
+        GCHECK(cudaMemcpyAsync(h.data(), b.wprof, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        GCHECK(cudaStreamSynchronize(st));
+        if (FILE* f = fopen(wprof_path, "wb")) {
+            const unsigned long long hdr[4] = {nwarps, grid, gbig, (unsigned long long)WPB};
+            fwrite(hdr, 8, 4, f);
+            fwrite(h.data(), 8, h.size(), f);
+            fclose(f);
+        }
+        cudaFreeAsync(b.wprof, st);
+    }
     if (sync_debug) {
         cudaError_t e = cudaStreamSynchronize(st);
         fprintf(stderr, "[girg] k_big<%d,%d,%d>: %s\n", D, SCHEME, (int)STATS, cudaGetErrorString(e));
@@ -797,12 +823,17 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         a.nitems = (unsigned int*)(misc + 28);
         a.stats = stats_out ? d_cnt : nullptr;
         a.err = d_err;
-        unsigned int items_cap = std::max<unsigned int>(1u << 14, n32 / 64);
+        unsigned int items_cap = std::max<unsigned int>(1u << 16, n32 / 4);
         a.items = S.alloc<BigItem>(items_cap);
         a.items_cap = items_cap;
         a.nP = K + 1;
         a.ntab = (unsigned)hp.tab.size();
         a.ntasks = (unsigned)hp.tasks.size();
+        a.big_work = BIG_WORK;
+        a.item_work = ITEM_WORK;
+        if (const char* e = getenv("GIRG_BIG_WORK")) a.big_work = strtoull(e, nullptr, 10);
+        if (const char* e = getenv("GIRG_ITEM_WORK")) a.item_work = strtoull(e, nullptr, 10);
+        a.wprof = nullptr;
         PE.record(2, st);
         char hmisc[256];
         for (int attempt = 0;; ++attempt) {
@@ -856,6 +887,8 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
             stats_out->edges2 = hc.edges2;
             stats_out->neartie1 = hc.nt1;
             stats_out->neartie2 = hc.nt2;
+            stats_out->fast_fallback = hc.fb;
+            stats_out->fast_mismatch = hc.mm;
             stats_out->layers = (uint64_t)hp.p.L;
             stats_out->key_space = K;
         }

@@ -139,4 +139,62 @@ __device__ __forceinline__ double prob_uv(double wu, double wv, double s, double
     return pow(ratio, invT);
 }
 
+// ---------------------------------------------------------------------------------------
+// Fast decisions.  Each returns a decision only when it provably
+// equals the one of the canonical double-precision arithmetic above; otherwise it reports
+// "undecided" and the caller evaluates the canonical expression.  log2 of a double is taken as
+// exponent (exact) + MUFU lg2 of the top 23 mantissa bits: |error| <= 2^-20 + 2^-22.5 < 1.3e-6.
+// ---------------------------------------------------------------------------------------
+// log2(x) = e + f for a positive normal double; false for 0, subnormal, inf, nan
+__device__ __forceinline__ bool log2_split(double x, int& e, float& f)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    const int ex = (int)((b >> 52) & 0x7ffu);
+    e = ex - 1023;
+    f = __log2f(__int_as_float(0x3f800000 | (unsigned)((b >> 29) & 0x7fffffu)));
+    return ex != 0 && ex != 0x7ff && (b >> 63) == 0;
+}
+
+// r < min(1, ((wu*wv)*s / D)^invT) ?  1 / 0, or -1 when the float estimate cannot decide.
+// log2 ratio = sum of four log2_split terms (error <= 4 * 1.3e-6 + float rounding 7e-7 < 6e-6);
+// log2 r error <= 1.3e-6; margins 1e-5 (ratio vs 1) and 1e-5 * invT + 2e-6.
+__device__ __forceinline__ int fast_lt_prob(double r, double wu, double wv, double s, double Dp, double invT)
+{
+    int e1, e2, e3, e4, e5;
+    float f1, f2, f3, f4, f5;
+    bool ok = log2_split(wu, e1, f1);
+    ok &= log2_split(wv, e2, f2);
+    ok &= log2_split(s, e3, f3);
+    ok &= log2_split(Dp, e4, f4);
+    ok &= log2_split(r, e5, f5);
+    if (!ok) return -1;
+    const double lr = (double)(e1 + e2 + e3 - e4) + (double)((f1 + f2) + (f3 - f4));
+    if (lr > 1e-5) return 1;   // ratio > 1: p = 1 > r
+    if (lr > -1e-5) return -1;
+    const double diff = invT * lr - ((double)e5 + (double)f5);  // log2 p - log2 r
+    const double margin = 1e-5 * invT + 2e-6;
+    if (diff > margin) return 1;
+    if (diff < -margin) return 0;
+    return -1;
+}
+
+// geometric jump (R10): z = log(1-rj)/log1p(-pbar) = log2(y)/log2(1-pbar), y = 1-rj in (0,1),
+// il2 = 1/log2(1-pbar) < 0.  Returns 1: stop (z >= remaining), 0: land at skip k = floor(z),
+// -1: undecided.  |z error| <= 1.3e-6 |il2| (+ rounding): margin 2e-6 |il2| + 1e-12 z + 1e-12.
+__device__ __forceinline__ int fast_jump(double y, double il2, long long remaining, long long& k)
+{
+    int e;
+    float f;
+    if (!log2_split(y, e, f)) return -1;
+    const double z = ((double)e + (double)f) * il2;
+    const double margin = 2e-6 * fabs(il2) + 1e-12 * z + 1e-12;
+    const double rem = (double)remaining;
+    if (z - margin >= rem) return 1;
+    if (z + margin >= rem) return -1;
+    const double lo = floor(z - margin), hi = floor(z + margin);
+    if (lo != hi || lo < 0.0) return -1;
+    k = (long long)lo;
+    return 0;
+}
+
 }  // namespace girg

@@ -1,26 +1,29 @@
-// sample.cuh -- K5: the GIRG sampling kernels (v4), included by girg.cu inside namespace girg.
+// sample.cuh -- K5: the GIRG sampling kernels (v5), included by girg.cu inside namespace girg.
 //
 // Events (Algorithm 1; R2, R16): for a layer pair i <= j, a neighbouring cell pair
 // (A, B) on level CL(i,j) is a type-I event (every candidate tested, Alg. 1 line 3), a distant
 // cell pair with neighbouring parents on a level 2 <= l <= CL(i,j) is a type-II event (geometric
-// jumps under the bound pbar, Alg. 1 lines 5-6).  Every event of a level-l cell A
-// lies inside the "region" of A's parent: the 2^d children of the 3^d neighbours of parent(A)
-// (all cells of level l when l <= 2).
+// jumps under the bound pbar, Alg. 1 lines 5-6).
 //
 // Work decomposition:
-//   * task = (layer i, partner j, level l, parent cell Cpar of layer i on level l-1).  It is
-//     owned by the first sorted point of Cpar, so every nonempty parent is visited exactly once
-//     per (j, l); host tables list the tasks of a point by (layer, first level lf).
-//   * one warp per task: lanes load the region's Lemma-1 ranges (P entries) once for the up to
-//     2^d children A of Cpar, classify the region's cells per child (kind 0: neighbour / type-I,
-//     kind 1: distant with delta_max = 2, kind 2: delta_max = 3) as bit masks, and prefix-sum
-//     the per-parent counts in Morton order.
+//   * job = (layer i, partner j, level l, task cell Cg of layer i on level lg = max(0, l - G)):
+//     the level-l descendants A of Cg ("children") against the "region" = the level-l
+//     descendants of the 3^d neighbours of Cg (of all level-lg cells when lg <= 1), which holds
+//     every neighbour and every distant cell with neighbouring parents of each child.  A job is
+//     owned by the first sorted point of Cg; host tables list the jobs of a point by (layer,
+//     first level lf).  G = 3 for d = 1 (8 children per job), else 1.
+//   * one warp per job: lanes load the region's Lemma-1 ranges (P entries) once, classify every
+//     (child, region parent) pair in parallel into bit masks of kinds (0: neighbour / type-I,
+//     1: distant with delta_max = 2, 2: delta_max = 3), and prefix-sum the counts in Morton
+//     order of the region cells.
 //   * units: a type-I candidate pair, or one chunk (jump chain) of a type-II sequence.  A
 //     sequence is one distant cell pair (scheme EVENT, Alg. 1 as written) or the concatenation of
-//     all distant cells of A with the same bound class (scheme MERGED, R22).  Lanes pull units
-//     dynamically and advance one Philox draw / one candidate per step, so jump chains of
-//     different lengths do not serialise the warp.
-//   * tasks with too much work are split into unit-range items of a global queue (k_big).
+//     all distant cells of A with the same bound class (scheme MERGED, R22).
+//   * engine: NSLOT job slots per warp.  Lanes pull units of the dispatch slot and advance one
+//     Philox draw / one candidate per step; when the dispatch slot runs dry the warp sets up the
+//     next job in a slot no lane is still working on, while lanes finish earlier jobs' chains,
+//     so jobs pipeline and short jobs do not leave the warp idle.
+//   * jobs with too much work are split into unit-range items of a global queue (k_big).
 //   * edges are staged per warp in shared memory and written with one atomic per flush.
 #pragma once
 
@@ -42,27 +45,46 @@
 
 constexpr int SCHEME_EVENT = 0, SCHEME_MERGED = 1;
 constexpr int EB = 256;                          // staged edges per warp
-constexpr unsigned long long BIG_WORK = 24576;   // weighted units above which a batch is queued
-constexpr unsigned long long ITEM_WORK = 6144;   // weighted units per queued item
+constexpr unsigned long long BIG_WORK = 1024;    // weighted units above which a job is queued
+constexpr unsigned long long ITEM_WORK = 512;    // weighted units per queued item
 constexpr int ERR_ITEMS = 16;
+constexpr unsigned FULL = 0xffffffffu;
 
 template <int D>
 struct Geo {
     static constexpr int G = D == 1 ? 3 : 1;                 // levels between a task cell and its children
     static constexpr int NCH = 1 << (D * G);                 // children (= sub-cells per region parent)
     static constexpr int NPAR = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : 243;  // 3^d
-    static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // level-1 tasks: all 2^d level-1 cells
-    static constexpr int CB = D <= 3 ? NCH : (D == 4 ? 4 : 2);        // children per batch
-    static constexpr int WPB = D <= 3 ? 8 : (D == 4 ? 4 : 2);         // warps per block
-    static constexpr int MINB = D <= 2 ? 4 : (D == 3 ? 3 : 1);        // resident blocks per SM (register cap)
+    static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // lg = 1: all 2^d level-1 cells
+    static constexpr int CB = D <= 3 ? NCH : (D == 4 ? 4 : 2);        // children per job (batch)
+    static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? 4 : 2);         // warps per block
+    static constexpr int MINB = D <= 2 ? 3 : (D == 3 ? 3 : 1);        // resident blocks per SM (register cap)
+    static constexpr int NSLOT = D <= 2 ? 4 : (D == 3 ? 3 : 2);       // job slots per warp (pipeline depth)
     static constexpr int RECW = D == 1 ? 2 : (D <= 3 ? 4 : 6);       // doubles per point record
 };
 
-struct Counters {
-    unsigned long long cand1, ev2, chunks, draws, landings, edges1, edges2, nt1, nt2;
+template <int N>
+struct MaskOf {
+    using T = uint32_t;
+};
+template <>
+struct MaskOf<8> {
+    using T = uint8_t;
+};
+template <>
+struct MaskOf<4> {
+    using T = uint8_t;
+};
+template <>
+struct MaskOf<16> {
+    using T = uint16_t;
 };
 
-// one (child, kind) sequence of a batch
+struct Counters {
+    unsigned long long cand1, ev2, chunks, draws, landings, edges1, edges2, nt1, nt2, fb, mm;
+};
+
+// one (child, kind) sequence of a job
 struct Seq {
     unsigned long long units;  // candidates (kind 0) or chunks (kinds 1, 2)
     unsigned long long N;      // merged: nA * M
@@ -73,9 +95,9 @@ struct Seq {
 
 struct BigItem {
     uint32_t Cpar;
-    uint16_t task;     // j | l<<6 | t1<<12 | t2<<13
+    uint16_t task;  // j | l<<6 | t1<<12 | t2<<13
     uint8_t i, batch;
-    unsigned long long lo, hi;  // unit range of the batch
+    unsigned long long lo, hi;  // unit range of the job
 };
 
 struct SampleArgs {
@@ -99,19 +121,43 @@ struct SampleArgs {
     int* err;
     unsigned long long nP;
     unsigned int ntab, ntasks;
+    unsigned long long big_work, item_work;  // job split thresholds (BIG_WORK / ITEM_WORK by default)
+    unsigned long long* wprof;               // optional per-warp profile: cycles, jobs, iterations, lane steps
+};
+
+struct TaskDesc {
+    int i, j, l, t1, t2;
+    uint32_t Cpar;     // the task cell Cg, on level lg = max(0, l - G)
+    int lg, npar, cs;  // task level, region parents, child shift d (l - lg)
+};
+
+// per-job constants read by the lanes
+struct JobInfo {
+    double pbar[2], Lbar[2];  // type-II bounds of kinds 1, 2 (R9)
+    double il2[2];            // 1 / log2(1 - pbar) (fast jump path)
+    int clog2[2];             // EVENT chunk length (R10)
+    uint32_t tag;             // l | i<<5 | j<<11
+    int npar, cs, same_layer;
+};
+
+template <int D>
+struct Slot {
+    static constexpr int NPAR = Geo<D>::MAXPAR, NCH = Geo<D>::NCH, CB = Geo<D>::CB;
+    using MaskT = typename MaskOf<NCH>::T;
+    uint32_t par[NPAR];              // region parent codes on level lg, Morton order
+    uint32_t rstart[NPAR][NCH + 1];  // sorted positions of the region sub-cells (layer j)
+    uint32_t achild[NCH + 1];        // sorted positions of Cg's children (layer i)
+    uint32_t pre[CB][3][NPAR + 1];   // per (child, kind): prefix over parents (candidates / chunks)
+    MaskT mask[CB][3][NPAR];         // per (child, kind, parent): sub-cells of that kind
+    Seq seq[CB][3];
+    unsigned long long uoff[CB * 3 + 1];  // unit offsets of the (child, kind) sequences
+    JobInfo job;
+    uint8_t child[NCH];  // nonempty owned children of Cg
 };
 
 template <int D>
 struct WarpSmem {
-    static constexpr int NPAR = Geo<D>::MAXPAR, NCH = Geo<D>::NCH, CB = Geo<D>::CB;
-    uint32_t par[NPAR];                   // region parent codes on level l-1, Morton order
-    uint32_t rstart[NPAR][NCH + 1];       // sorted positions of the region sub-cells (layer j)
-    uint32_t achild[NCH + 1];             // sorted positions of Cpar's children (layer i)
-    uint32_t pre[CB][3][NPAR + 1];        // per (child, kind): prefix over parents (candidates / chunks)
-    uint32_t mask[CB][3][NPAR];           // per (child, kind, parent): sub-cells of that kind
-    Seq seq[CB][3];
-    unsigned long long uoff[CB * 3 + 1];  // unit offsets of the (child, kind) sequences
-    uint8_t child[NCH];                   // nonempty owned children of Cpar
+    Slot<D> slot[Geo<D>::NSLOT];
     uint2 ebuf[EB];
 };
 
@@ -120,16 +166,40 @@ struct WarpSmem {
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+__device__ __forceinline__ unsigned long long shfl_up64(unsigned long long v, int o)
+{
+    const uint32_t lo = __shfl_up_sync(FULL, (uint32_t)v, o), hi = __shfl_up_sync(FULL, (uint32_t)(v >> 32), o);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
+__device__ __forceinline__ unsigned long long shfl64(unsigned long long v, int src)
+{
+    const uint32_t lo = __shfl_sync(FULL, (uint32_t)v, src), hi = __shfl_sync(FULL, (uint32_t)(v >> 32), src);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
+// inclusive warp scan of 64-bit values
+__device__ __forceinline__ unsigned long long warp_incl_scan64(unsigned long long v)
+{
+    const unsigned lane = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = shfl_up64(v, o);
+        if (lane >= (unsigned)o) v += y;
+    }
+    return v;
+}
+
 __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t& total)
 {
     const unsigned lane = lane_id();
     uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        const uint32_t y = __shfl_up_sync(FULL, x, o);
         if (lane >= (unsigned)o) x += y;
     }
-    total = __shfl_sync(0xffffffffu, x, 31);
+    total = __shfl_sync(FULL, x, 31);
     return x - v;
 }
 
@@ -138,7 +208,7 @@ __device__ __forceinline__ void warp_flush(const SampleArgs& a, uint2* buf, unsi
     __syncwarp();
     unsigned long long base = 0;
     if (lane_id() == 0 && fill) base = atomicAdd(a.m, (unsigned long long)fill);
-    base = __shfl_sync(0xffffffffu, base, 0);
+    base = shfl64(base, 0);
     for (unsigned k = lane_id(); k < fill; k += 32) {
         const unsigned long long slot = base + k;
         if (slot < a.cap) a.edges[slot] = buf[k];
@@ -151,7 +221,7 @@ __device__ __forceinline__ void warp_flush(const SampleArgs& a, uint2* buf, unsi
 __device__ __forceinline__ void warp_emit(const SampleArgs& a, uint2* buf, unsigned& fill, bool edge, uint32_t u,
                                           uint32_t v)
 {
-    const unsigned em = __ballot_sync(0xffffffffu, edge);
+    const unsigned em = __ballot_sync(FULL, edge);
     if (!em) return;
     const unsigned cnt = __popc(em);
     if (fill + cnt > (unsigned)EB) warp_flush(a, buf, fill);
@@ -176,109 +246,6 @@ __device__ __forceinline__ void load_rec(const SampleArgs& a, uint32_t p, double
     w = v[D];
 }
 
-// torus cell gap on level l per dimension, max over dimensions (R8): delta_max(A, B)
-template <int D>
-__device__ __forceinline__ int delta_max_cells(const uint32_t (&ac)[D], uint32_t B, int l)
-{
-    if (l == 0) return 0;
-    uint32_t bc[D];
-    morton_decode<D>(B, bc);
-    const uint32_t side = 1u << l;
-    int dm = 0;
-#pragma unroll
-    for (int k = 0; k < D; ++k) {
-        const uint32_t g = ac[k] > bc[k] ? ac[k] - bc[k] : bc[k] - ac[k];
-        dm = max(dm, (int)min(g, side - g));
-    }
-    return dm;
-}
-
-// ---------------------------------------------------------------------------------------
-// task setup: region parents, their sub-cell ranges in layer j, Cpar's children in layer i
-// ---------------------------------------------------------------------------------------
-struct TaskDesc {
-    int i, j, l, t1, t2;
-    uint32_t Cpar;  // the task cell, on level lg = max(0, l - G)
-    int lg, npar, cs;  // task level, region parents, child shift d (l - lg)
-};
-
-template <int D>
-__device__ __forceinline__ void setup_task(const SampleArgs& a, WarpSmem<D>& W, const TaskDesc& t, int& nchild)
-{
-    constexpr int NCH = Geo<D>::NCH;
-    const Plan* pl = a.pl;
-    const unsigned lane = lane_id();
-    const int nsub = 1 << t.cs;
-    // region parents in Morton order
-    if (t.lg >= 2) {
-        const int lam = t.lg;
-        uint32_t pc[D];
-        morton_decode<D>(t.Cpar, pc);
-        const uint32_t mask = (1u << lam) - 1u;
-        for (int q = lane; q < t.npar; q += 32) {
-            uint32_t c[D];
-            int r = q;
-#pragma unroll
-            for (int k = D - 1; k >= 0; --k) {  // offsets in {-1,0,1}^d (any fixed order; sorted below)
-                c[k] = (pc[k] + (uint32_t)(r % 3) - 1u) & mask;
-                r /= 3;
-            }
-            W.par[q] = morton_encode<D>(c);
-        }
-        __syncwarp();
-        // rank sort (codes are distinct on levels >= 2)
-        uint32_t mine[(Geo<D>::MAXPAR + 31) / 32];
-        int rk[(Geo<D>::MAXPAR + 31) / 32];
-#pragma unroll
-        for (int s = 0; s < (Geo<D>::MAXPAR + 31) / 32; ++s) {
-            const int q = lane + 32 * s;
-            rk[s] = 0;
-            mine[s] = q < t.npar ? W.par[q] : 0u;
-            if (q < t.npar)
-                for (int o = 0; o < t.npar; ++o) rk[s] += W.par[o] < mine[s];
-        }
-        __syncwarp();
-#pragma unroll
-        for (int s = 0; s < (Geo<D>::MAXPAR + 31) / 32; ++s) {
-            const int q = lane + 32 * s;
-            if (q < t.npar) W.par[rk[s]] = mine[s];
-        }
-    } else {
-        for (int q = lane; q < t.npar; q += 32) W.par[q] = (uint32_t)q;  // lg = 1: all level-1 cells; lg = 0: root
-    }
-    __syncwarp();
-    // Lemma-1 ranges of the region sub-cells in layer j and of Cpar's children in layer i
-    const int shj = D * ((int)pl->I[t.j] - t.l), shi = D * ((int)pl->I[t.i] - t.l);
-    const uint32_t bj = pl->base[t.j], bi = pl->base[t.i];
-    const int per = nsub + 1;
-    for (int e = lane; e < t.npar * per; e += 32) {
-        const int q = e / per, k = e - q * per;
-        const unsigned long long cell = ((unsigned long long)W.par[q] << t.cs) + (unsigned)k;
-        GCHK(bj + (cell << shj) < a.nP);
-        W.rstart[q][k] = __ldg(&a.P[bj + (cell << shj)]);
-    }
-    for (int k = lane; k <= nsub; k += 32) {
-        const unsigned long long cell = ((unsigned long long)t.Cpar << t.cs) + (unsigned)k;
-        GCHK(bi + (cell << shi) < a.nP);
-        W.achild[k] = __ldg(&a.P[bi + (cell << shi)]);
-    }
-    __syncwarp();
-    // nonempty children owned by this shard (ownership by the A cell's block)
-    bool ok = false;
-    if ((int)lane < nsub) {
-        ok = W.achild[lane + 1] > W.achild[lane];
-        const uint32_t A = (t.Cpar << t.cs) + lane;
-        const unsigned long long b = t.l >= pl->sl ? ((unsigned long long)A >> (D * (t.l - pl->sl)))
-                                                   : ((unsigned long long)A << (D * (pl->sl - t.l)));
-        ok = ok && b >= pl->blo && b < pl->bhi;
-    }
-    const unsigned bm = __ballot_sync(0xffffffffu, ok);
-    if (ok) W.child[__popc(bm & ((1u << lane) - 1u))] = (uint8_t)lane;
-    nchild = __popc(bm);
-    (void)NCH;
-    __syncwarp();
-}
-
 // chunk length (log2) of a type-II sequence of N candidates with table log2 length c0 and a
 // cap of 2^capbits chunks (R10 / R22)
 __device__ __forceinline__ int chunk_log2(unsigned long long N, int c0, int capbits)
@@ -288,136 +255,263 @@ __device__ __forceinline__ int chunk_log2(unsigned long long N, int c0, int capb
     return c;
 }
 
-// kind of region sub-cell B relative to child A (-1: none): 0 neighbours (type-I), 1 / 2 distant
-// with neighbouring parents and delta_max = 2 / 3 (type-II)
 template <int D>
-__device__ __forceinline__ int kind_of(const TaskDesc& t, const uint32_t (&ac)[D], uint32_t A, uint32_t B)
+__device__ __forceinline__ TaskDesc make_task(int i, uint16_t task, uint32_t Cpar)
 {
-    const int dm = delta_max_cells<D>(ac, B, t.l);
-    if (dm <= 1) return (t.t1 && (t.i < t.j || B >= A)) ? 0 : -1;
-    if (!t.t2 || (t.i == t.j && B <= A)) return -1;
-    if (Geo<D>::G > 1 && t.l >= 3) {  // the region spans more than parent(A)'s neighbours
-        uint32_t pa[D];
-#pragma unroll
-        for (int k = 0; k < D; ++k) pa[k] = ac[k] >> 1;
-        if (delta_max_cells<D>(pa, B >> D, t.l - 1) > 1) return -1;
-    }
-    return dm - 1;  // 1: delta_max = 2, 2: delta_max = 3
+    TaskDesc t;
+    t.i = i;
+    t.j = task & 63;
+    t.l = (task >> 6) & 63;
+    t.t1 = (task >> 12) & 1;
+    t.t2 = (task >> 13) & 1;
+    t.Cpar = Cpar;
+    t.lg = max(0, t.l - Geo<D>::G);
+    t.cs = D * (t.l - t.lg);
+    t.npar = t.lg >= 2 ? Geo<D>::NPAR : (t.lg == 1 ? (1 << D) : 1);
+    return t;
 }
 
-// per-batch setup: masks, per-parent prefix counts, sequences and unit offsets
+// ---------------------------------------------------------------------------------------
+// job setup (warp-collective): region, children, classification, sequences, unit offsets.
+// Out of line (called once per job, keeps the engine loop's register allocation small).
+// ---------------------------------------------------------------------------------------
+struct JobSetup {
+    unsigned long long U;     // units of the job
+    unsigned long long work;  // weighted units (a chunk counts 8)
+    int nchild;               // nonempty owned children of the task cell (all batches)
+    int nseq2;                // nonempty type-II sequences (counter)
+};
+
 template <int D, int SCHEME>
-__device__ __forceinline__ unsigned long long setup_batch(const SampleArgs& a, WarpSmem<D>& W, const TaskDesc& t,
-                                                          int c0, int nc, unsigned long long& work)
+__device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, const TaskDesc t, int batch)
 {
+    JobSetup out = {0ull, 0ull, 0, 0};
+    constexpr int NCH = Geo<D>::NCH, CB = Geo<D>::CB;
+    using MaskT = typename Slot<D>::MaskT;
+    const Plan* pl = a.pl;
     const unsigned lane = lane_id();
     const int nsub = 1 << t.cs;
-    const TabEntry* te = t.t2 ? a.tab + (a.pl->tab_off[t.i * MAXL + t.j] + 2u * (uint32_t)(t.l - 2)) : nullptr;
-    unsigned long long wk = 0;
-    for (int cc = 0; cc < nc; ++cc) {
-        const int e = W.child[c0 + cc];
-        const uint32_t A = (t.Cpar << t.cs) + (uint32_t)e;
-        uint32_t ac[D];
-        morton_decode<D>(A, ac);
-        const uint32_t a0 = W.achild[e], nA = W.achild[e + 1] - a0;
-        uint32_t base[3] = {0u, 0u, 0u};
-        for (int q0 = 0; q0 < t.npar; q0 += 32) {
-            const int q = q0 + (int)lane;
-            uint32_t cnt[3] = {0u, 0u, 0u}, m[3] = {0u, 0u, 0u};
-            if (q < t.npar) {
-                for (int s = 0; s < nsub; ++s) {
-                    const uint32_t B = (W.par[q] << t.cs) + (uint32_t)s;
-                    const int k = kind_of<D>(t, ac, A, B);
-                    if (k < 0) continue;
-                    const uint32_t nB = W.rstart[q][s + 1] - W.rstart[q][s];
+    // ---- region parents in Morton order ----
+    if (t.lg >= 2) {
+        uint32_t pc[D];
+        morton_decode<D>(t.Cpar, pc);
+        const uint32_t mask = (1u << t.lg) - 1u;
+        for (int q = lane; q < t.npar; q += 32) {
+            uint32_t c[D];
+            int r = q;
 #pragma unroll
-                    for (int kk = 0; kk < 3; ++kk) {
-                        if (kk != k) continue;
-                        m[kk] |= 1u << s;
-                        if (kk == 0 || SCHEME == SCHEME_MERGED) {
-                            cnt[kk] += nB;
-                        } else if (nB) {  // EVENT: chunks of the event (A, B)
-                            const unsigned long long N = (unsigned long long)nA * nB;
-                            const TabEntry& tk = te[kk - 1];
-                            if (tk.pbar > 0.0) cnt[kk] += (uint32_t)(((N - 1) >> chunk_log2(N, tk.clog2, 15)) + 1);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int kk = 0; kk < 3; ++kk) W.mask[cc][kk][q] = m[kk];
+            for (int k = D - 1; k >= 0; --k) {  // offsets in {-1,0,1}^d (distinct for lg >= 2; sorted below)
+                c[k] = (pc[k] + (uint32_t)(r % 3) - 1u) & mask;
+                r /= 3;
             }
-#pragma unroll
-            for (int kk = 0; kk < 3; ++kk) {
-                uint32_t tot;
-                const uint32_t ex = warp_excl_scan(cnt[kk], tot);
-                if (q < t.npar) W.pre[cc][kk][q] = base[kk] + ex;
-                base[kk] += tot;
-            }
+            S.par[q] = morton_encode<D>(c);
         }
-        if (lane < 3) {
-            const int k = (int)lane;
-            const uint32_t M = k == 0 ? base[0] : (k == 1 ? base[1] : base[2]);
-            W.pre[cc][k][t.npar] = M;
-            Seq& S = W.seq[cc][k];
-            S.A = A;
-            S.a0 = a0;
-            S.nA = nA;
-            S.M = M;
-            S.cl2 = 0;
-            S.N = 0;
-            unsigned long long units = 0;
-            if (k == 0) {
-                units = (unsigned long long)nA * M;
-            } else if (SCHEME == SCHEME_EVENT) {
-                units = M;
-            } else if (M) {
-                const TabEntry& tk = te[k - 1];
-                if (tk.pbar > 0.0) {
-                    S.N = (unsigned long long)nA * M;
-                    S.cl2 = chunk_log2(S.N, tk.clog2m, 32);
-                    units = ((S.N - 1) >> S.cl2) + 1;
-                }
+        __syncwarp();
+        constexpr int NS = (Geo<D>::MAXPAR + 31) / 32;
+        uint32_t mine[NS];
+        int rk[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {  // rank sort
+            const int q = lane + 32 * s;
+            rk[s] = 0;
+            mine[s] = q < t.npar ? S.par[q] : 0u;
+            if (q < t.npar)
+                for (int o = 0; o < t.npar; ++o) rk[s] += S.par[o] < mine[s];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const int q = lane + 32 * s;
+            if (q < t.npar) S.par[rk[s]] = mine[s];
+        }
+    } else {
+        for (int q = lane; q < t.npar; q += 32) S.par[q] = (uint32_t)q;  // lg = 1: all level-1 cells; lg = 0: root
+    }
+    __syncwarp();
+    // ---- Lemma-1 ranges of the region sub-cells (layer j) and of Cg's children (layer i) ----
+    {
+        const int shj = D * ((int)pl->I[t.j] - t.l), shi = D * ((int)pl->I[t.i] - t.l);
+        const uint32_t bj = pl->base[t.j], bi = pl->base[t.i];
+        const int per = nsub + 1;
+        for (int e = lane; e < t.npar * per + per; e += 32) {
+            if (e < t.npar * per) {
+                const int q = e / per, k = e - q * per;
+                const unsigned long long cell = ((unsigned long long)S.par[q] << t.cs) + (unsigned)k;
+                GCHK(bj + (cell << shj) < a.nP);
+                S.rstart[q][k] = __ldg(&a.P[bj + (cell << shj)]);
+            } else {
+                const int k = e - t.npar * per;
+                const unsigned long long cell = ((unsigned long long)t.Cpar << t.cs) + (unsigned)k;
+                GCHK(bi + (cell << shi) < a.nP);
+                S.achild[k] = __ldg(&a.P[bi + (cell << shi)]);
             }
-            S.units = units;
-            wk += units * (k == 0 ? 1ull : 8ull);
         }
     }
-#pragma unroll
-    for (int o = 1; o < 4; o <<= 1) wk += __shfl_xor_sync(0xffffffffu, wk, o);
     __syncwarp();
+    // ---- nonempty children owned by this shard (ownership by the A cell's block) ----
+    {
+        int cnt = 0;
+        for (int c0 = 0; c0 < nsub; c0 += 32) {
+            const int e = c0 + (int)lane;
+            bool ok = false;
+            if (e < nsub) {
+                ok = S.achild[e + 1] > S.achild[e];
+                const uint32_t A = (t.Cpar << t.cs) + (uint32_t)e;
+                const unsigned long long b = t.l >= pl->sl ? ((unsigned long long)A >> (D * (t.l - pl->sl)))
+                                                           : ((unsigned long long)A << (D * (pl->sl - t.l)));
+                ok = ok && b >= pl->blo && b < pl->bhi;
+            }
+            const unsigned bm = __ballot_sync(FULL, ok);
+            const int rank = cnt + __popc(bm & ((1u << lane) - 1u));
+            if (ok && rank >= batch * CB && rank < (batch + 1) * CB) S.child[rank - batch * CB] = (uint8_t)e;
+            cnt += __popc(bm);
+        }
+        out.nchild = cnt;
+    }
+    const int nc = min(CB, out.nchild - batch * CB);
+    if (nc <= 0) return out;
+    const TabEntry* te = t.t2 ? a.tab + (pl->tab_off[t.i * MAXL + t.j] + 2u * (uint32_t)(t.l - 2)) : nullptr;
     if (lane == 0) {
-        unsigned long long acc = 0;
-        for (int s = 0; s < nc * 3; ++s) {
-            W.uoff[s] = acc;
-            acc += W.seq[s / 3][s % 3].units;
+        JobInfo& J = S.job;
+        J.tag = (uint32_t)t.l | ((uint32_t)t.i << 5) | ((uint32_t)t.j << 11);
+        J.npar = t.npar;
+        J.cs = t.cs;
+        J.same_layer = t.i == t.j;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            J.pbar[k] = te ? te[k].pbar : 0.0;
+            J.Lbar[k] = te ? te[k].Lbar : 0.0;
+            J.il2[k] = te ? te[k].il2 : 0.0;
+            J.clog2[k] = te ? te[k].clog2 : 0;
         }
-        W.uoff[nc * 3] = acc;
     }
     __syncwarp();
-    work = __shfl_sync(0xffffffffu, wk, 0);
-    return W.uoff[nc * 3];
+    // ---- phase 1: classify every (child, region parent) pair in parallel ----
+    const int subl = t.cs / D;  // levels between a region parent and its sub-cells
+    const uint32_t side = 1u << t.l, msk = side - 1u;
+    const uint32_t side2 = side >> 1, msk2 = side2 - 1u;  // level l-1 (parent check, G > 1)
+    const bool pcheck = Geo<D>::G > 1 && t.l >= 3;
+    for (int idx = lane; idx < nc * t.npar; idx += 32) {
+        const int cc = idx / t.npar, q = idx - cc * t.npar;
+        const int e = S.child[cc];
+        const uint32_t A = (t.Cpar << t.cs) + (uint32_t)e;
+        uint32_t ac[D], pc[D];
+        morton_decode<D>(A, ac);
+        morton_decode<D>(S.par[q], pc);
+        const uint32_t nA = S.achild[e + 1] - S.achild[e];
+        uint32_t cnt[3] = {0u, 0u, 0u};
+        uint32_t m[3] = {0u, 0u, 0u};
+#pragma unroll
+        for (int s = 0; s < NCH; ++s) {
+            if (s >= nsub) break;
+            uint32_t so[D];
+            morton_decode<D>((uint32_t)s, so);
+            uint32_t dm = 0, dp = 0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const uint32_t bk = ((pc[k] << subl) + so[k]) & msk;
+                const uint32_t df = (bk - ac[k]) & msk;
+                dm = max(dm, min(df, side - df));
+                if (pcheck) {
+                    const uint32_t df2 = ((bk >> 1) - (ac[k] >> 1)) & msk2;
+                    dp = max(dp, min(df2, side2 - df2));
+                }
+            }
+            const uint32_t B = (S.par[q] << t.cs) + (uint32_t)s;
+            int kind = -1;
+            if (dm <= 1) {
+                if (t.t1 && (t.i < t.j || B >= A)) kind = 0;
+            } else if (t.t2 && dp <= 1 && (t.i < t.j || B > A)) {
+                kind = (int)dm - 1;  // 1: delta_max = 2, 2: delta_max = 3
+            }
+            if (kind < 0) continue;
+            const uint32_t nB = S.rstart[q][s + 1] - S.rstart[q][s];
+            uint32_t add = nB;
+            if (SCHEME == SCHEME_EVENT && kind > 0) {  // chunks of the event (A, B)
+                add = 0;
+                if (nB && te[kind - 1].pbar > 0.0) {
+                    const unsigned long long N = (unsigned long long)nA * nB;
+                    add = (uint32_t)(((N - 1) >> chunk_log2(N, te[kind - 1].clog2, 15)) + 1);
+                }
+            }
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk)
+                if (kk == kind) {
+                    m[kk] |= 1u << s;
+                    cnt[kk] += add;
+                }
+        }
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+            S.mask[cc][kk][q] = (MaskT)m[kk];
+            S.pre[cc][kk][q] = cnt[kk];
+        }
+    }
+    __syncwarp();
+    // ---- phase 2: per (child, kind): prefix over parents and the sequence ----
+    unsigned long long units = 0;
+    if ((int)lane < nc * 3) {
+        const int cc = (int)lane / 3, k = (int)lane - 3 * cc;
+        uint32_t acc = 0;
+        for (int q = 0; q < t.npar; ++q) {
+            const uint32_t c = S.pre[cc][k][q];
+            S.pre[cc][k][q] = acc;
+            acc += c;
+        }
+        S.pre[cc][k][t.npar] = acc;
+        const int e = S.child[cc];
+        Seq& Q = S.seq[cc][k];
+        Q.A = (t.Cpar << t.cs) + (uint32_t)e;
+        Q.a0 = S.achild[e];
+        Q.nA = S.achild[e + 1] - Q.a0;
+        Q.M = acc;
+        Q.cl2 = 0;
+        Q.N = 0;
+        if (k == 0) {
+            units = (unsigned long long)Q.nA * acc;
+        } else if (SCHEME == SCHEME_EVENT) {
+            units = acc;
+        } else if (acc && te[k - 1].pbar > 0.0) {
+            Q.N = (unsigned long long)Q.nA * acc;
+            Q.cl2 = chunk_log2(Q.N, te[k - 1].clog2m, 32);
+            units = ((Q.N - 1) >> Q.cl2) + 1;
+        }
+        Q.units = units;
+    }
+    out.nseq2 = __popc(__ballot_sync(FULL, ((int)lane % 3) != 0 && units != 0));
+    // ---- phase 3: unit offsets and weighted work ----
+    const unsigned long long incl = warp_incl_scan64(units);
+    if ((int)lane < nc * 3) S.uoff[lane + 1] = incl;
+    if (lane == 0) S.uoff[0] = 0;
+    unsigned long long wk = units * (((int)lane % 3) == 0 ? 1ull : 8ull);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wk += __shfl_xor_sync(FULL, wk, o);
+    out.work = wk;
+    out.U = shfl64(incl, nc * 3 - 1);
+    __syncwarp();
+    return out;
 }
 
 // concatenated index t (< M) of sequence (cc, k) -> sorted position in layer j and the cell
 template <int D>
-__device__ __forceinline__ uint32_t locate(const WarpSmem<D>& W, int npar, int cs, int cc, int k, uint32_t t,
+__device__ __forceinline__ uint32_t locate(const Slot<D>& S, int npar, int cs, int cc, int k, uint32_t t,
                                            uint32_t& B)
 {
     int lo = 0, hi = npar - 1;  // last parent with pre <= t
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (W.pre[cc][k][mid] <= t) lo = mid;
+        if (S.pre[cc][k][mid] <= t) lo = mid;
         else hi = mid - 1;
     }
-    uint32_t r = t - W.pre[cc][k][lo];
-    uint32_t m = W.mask[cc][k][lo];
+    uint32_t r = t - S.pre[cc][k][lo];
+    uint32_t m = S.mask[cc][k][lo];
     for (;;) {
         GCHK(m != 0);
         const int s = __ffs(m) - 1;
-        const uint32_t nB = W.rstart[lo][s + 1] - W.rstart[lo][s];
+        const uint32_t nB = S.rstart[lo][s + 1] - S.rstart[lo][s];
         if (r < nB) {
-            B = (W.par[lo] << cs) + (uint32_t)s;
-            return W.rstart[lo][s] + r;
+            B = (S.par[lo] << cs) + (uint32_t)s;
+            return S.rstart[lo][s] + r;
         }
         r -= nB;
         m &= m - 1u;
@@ -426,193 +520,36 @@ __device__ __forceinline__ uint32_t locate(const WarpSmem<D>& W, int npar, int c
 
 // EVENT scheme: chunk index u of sequence (cc, k) -> event (B, its range) and chunk within it
 template <int D>
-__device__ __forceinline__ void locate_event(const WarpSmem<D>& W, const TabEntry& tk, int npar, int cs, int cc,
-                                             int k, uint32_t nA, uint32_t u, uint32_t& B, uint32_t& b0,
-                                             uint32_t& nB, uint32_t& ch, int& cl2)
+__device__ __forceinline__ void locate_event(const Slot<D>& S, int clog2, int npar, int cs, int cc, int k,
+                                             uint32_t nA, uint32_t u, uint32_t& B, uint32_t& b0, uint32_t& nB,
+                                             uint32_t& ch, int& cl2)
 {
     int lo = 0, hi = npar - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (W.pre[cc][k][mid] <= u) lo = mid;
+        if (S.pre[cc][k][mid] <= u) lo = mid;
         else hi = mid - 1;
     }
-    uint32_t r = u - W.pre[cc][k][lo];
-    uint32_t m = W.mask[cc][k][lo];
+    uint32_t r = u - S.pre[cc][k][lo];
+    uint32_t m = S.mask[cc][k][lo];
     for (;;) {
         GCHK(m != 0);
         const int s = __ffs(m) - 1;
         m &= m - 1u;
-        const uint32_t nb = W.rstart[lo][s + 1] - W.rstart[lo][s];
+        const uint32_t nb = S.rstart[lo][s + 1] - S.rstart[lo][s];
         if (!nb) continue;
         const unsigned long long N = (unsigned long long)nA * nb;
-        const int c = chunk_log2(N, tk.clog2, 15);
+        const int c = chunk_log2(N, clog2, 15);
         const uint32_t nch = (uint32_t)(((N - 1) >> c) + 1);
         if (r < nch) {
-            B = (W.par[lo] << cs) + (uint32_t)s;
-            b0 = W.rstart[lo][s];
+            B = (S.par[lo] << cs) + (uint32_t)s;
+            b0 = S.rstart[lo][s];
             nB = nb;
             ch = r;
             cl2 = c;
             return;
         }
         r -= nch;
-    }
-}
-
-// ---------------------------------------------------------------------------------------
-// unit processing: lanes pull units of the batch's range [lo, hi) and advance one step each
-// ---------------------------------------------------------------------------------------
-template <int D, int SCHEME, bool STATS>
-__device__ __forceinline__ void run_units(const SampleArgs& a, WarpSmem<D>& W, const TaskDesc& t, int nc,
-                                          unsigned long long lo, unsigned long long hi, unsigned& fill,
-                                          Counters& C)
-{
-    const Plan* pl = a.pl;
-    const unsigned lane = lane_id();
-    const bool T0 = pl->T == 0.0;
-    const TabEntry* te = t.t2 ? a.tab + (pl->tab_off[t.i * MAXL + t.j] + 2u * (uint32_t)(t.l - 2)) : nullptr;
-    const uint32_t tag_base = (uint32_t)t.l | ((uint32_t)t.i << 5) | ((uint32_t)t.j << 11);
-    const bool same_layer = t.i == t.j;
-    unsigned long long next = lo;
-    bool busy = false;
-    int cc = 0, kind = 0;
-    // type-I unit state
-    uint32_t pa = 0, pb = 0, ua = 0, ub = 0;
-    // type-II chain state
-    long long pos = 0, end = 0;
-    uint32_t r = 0, ch = 0, Bev = 0, eb0 = 0, enB = 0;
-    for (;;) {
-        const unsigned idle = __ballot_sync(0xffffffffu, !busy);
-        if (next >= hi && idle == 0xffffffffu) break;
-        if (!busy && next < hi) {
-            const unsigned long long u = next + __popc(idle & ((1u << lane) - 1u));
-            if (u < hi) {
-                int s = 0;  // sequence holding unit u
-                while (W.uoff[s + 1] <= u) ++s;
-                cc = s / 3;
-                kind = s - 3 * cc;
-                const Seq& S = W.seq[cc][kind];
-                const unsigned long long x = u - W.uoff[s];
-                if (kind == 0) {
-                    const uint32_t si = (uint32_t)(x / S.M), ti = (uint32_t)(x - (unsigned long long)si * S.M);
-                    uint32_t B;
-                    pa = S.a0 + si;
-                    pb = locate<D>(W, t.npar, t.cs, cc, 0, ti, B);
-                    busy = !(same_layer && B == S.A && pb <= pa);  // same cell: only s < t (R16)
-                    if (busy && !T0) {
-                        ua = __ldg(&a.sid[pa]);
-                        ub = __ldg(&a.sid[pb]);
-                    }
-                } else {
-                    busy = true;
-                    r = 0;
-                    if (SCHEME == SCHEME_MERGED) {
-                        ch = (uint32_t)x;
-                        const unsigned long long st = x << S.cl2;
-                        pos = (long long)st - 1;
-                        end = (long long)min(S.N, st + (1ull << S.cl2));
-                    } else {
-                        int c2;
-                        locate_event<D>(W, te[kind - 1], t.npar, t.cs, cc, kind, S.nA, (uint32_t)x, Bev, eb0, enB,
-                                        ch, c2);
-                        const unsigned long long N = (unsigned long long)S.nA * enB;
-                        const unsigned long long st = (unsigned long long)ch << c2;
-                        pos = (long long)st - 1;
-                        end = (long long)min(N, st + (1ull << c2));
-                    }
-                    if (STATS) ++C.chunks;
-                }
-            }
-        }
-        next += __popc(idle);
-        // ---- one step ----
-        bool have = false, edge = false;
-        double ra = 0.0, pbar = 1.0;
-        uint4 o = make_uint4(0, 0, 0, 0);
-        if (busy && !T0) {
-            const Seq& S = W.seq[cc][kind];
-            uint4 ctr;
-            if (kind == 0) ctr = make_uint4(min(ua, ub), max(ua, ub), 0u, 3u);
-            else if (SCHEME == SCHEME_MERGED) ctr = make_uint4(S.A, ch, tag_base | ((uint32_t)(kind - 1) << 17) | (1u << 18), r);
-            else ctr = make_uint4(S.A, Bev, tag_base | (ch << 17), r);
-            o = philox4x32_10(ctr, a.k0, a.k1);
-        }
-        if (busy) {
-            if (kind == 0) {
-                have = true;
-            } else {
-                const Seq& S = W.seq[cc][kind];
-                const TabEntry& tk = te[kind - 1];
-                pbar = tk.pbar;
-                ++r;
-                if (STATS) ++C.draws;
-                const double rj = u53(o.x, o.y);
-                ra = u53(o.z, o.w);
-                const double z = pbar == 1.0 ? 0.0 : __ddiv_rn(log(__dsub_rn(1.0, rj)), tk.Lbar);
-                const long long remaining = end - pos - 1;
-                if (z >= (double)remaining) {
-                    busy = false;
-                } else {
-                    pos += 1 + (long long)z;
-                    have = true;
-                    if (STATS) ++C.landings;
-                    if (SCHEME == SCHEME_MERGED) {
-                        const unsigned long long g = (unsigned long long)pos;
-                        uint32_t si, ti;
-                        if (S.N <= 0xFFFFFFFFull) {
-                            si = (uint32_t)g / S.M;
-                            ti = (uint32_t)g - si * S.M;
-                        } else {
-                            si = (uint32_t)(g / S.M);
-                            ti = (uint32_t)(g - (unsigned long long)si * S.M);
-                        }
-                        uint32_t B;
-                        pa = S.a0 + si;
-                        pb = locate<D>(W, t.npar, t.cs, cc, kind, ti, B);
-                    } else {
-                        const unsigned long long g = (unsigned long long)pos;
-                        const uint32_t si = (uint32_t)(g / enB), ti = (uint32_t)(g - (unsigned long long)si * enB);
-                        pa = S.a0 + si;
-                        pb = eb0 + ti;
-                    }
-                }
-            }
-        }
-        if (have) {
-            double xu[D], xv[D], wu, wv;
-            load_rec<D>(a, pa, xu, wu);
-            load_rec<D>(a, pb, xv, wv);
-            const double Dp = dist_pow<D>(xu, xv);
-            if (T0) {
-                edge = Dp <= __dmul_rn(__dmul_rn(wu, wv), pl->s);
-            } else {
-                const double p = prob_uv(wu, wv, pl->s, Dp, pl->invT);
-                if (kind == 0) {
-                    const double r1 = u53(o.x, o.y);
-                    if (STATS && p < 1.0) C.nt1 += fabs(r1 - p) < 1e-12;
-                    edge = p >= 1.0 || r1 < p;
-                } else {
-                    const double rp = __dmul_rn(ra, pbar);
-                    if (STATS) C.nt2 += fabs(rp - p) < 1e-12 * pbar;
-                    edge = rp < p;
-                }
-            }
-            if (kind == 0) {
-                busy = false;
-                if (STATS) ++C.cand1;
-            }
-            if (edge) {
-                if (STATS) {
-                    if (kind == 0) ++C.edges1;
-                    else ++C.edges2;
-                }
-                if (kind != 0 || T0) {
-                    ua = __ldg(&a.sid[pa]);
-                    ub = __ldg(&a.sid[pb]);
-                }
-            }
-        }
-        warp_emit(a, W.ebuf, fill, edge, ua, ub);
     }
 }
 
@@ -629,85 +566,64 @@ __device__ __forceinline__ void flush_counters(const SampleArgs& a, const Counte
     atomicAdd(&a.stats->edges2, c.edges2);
     atomicAdd(&a.stats->nt1, c.nt1);
     atomicAdd(&a.stats->nt2, c.nt2);
+    atomicAdd(&a.stats->fb, c.fb);
+    atomicAdd(&a.stats->mm, c.mm);
 }
 
-template <int D>
-__device__ __forceinline__ TaskDesc make_task(const Plan* pl, int i, uint16_t task, uint32_t Cpar)
+// queue a job's unit range as items of ~ITEM_WORK weighted units (lane 0)
+__device__ __forceinline__ void push_items(const SampleArgs& a, const TaskDesc& t, uint16_t task, int batch,
+                                           unsigned long long U, unsigned long long work)
 {
-    TaskDesc t;
-    t.i = i;
-    t.j = task & 63;
-    t.l = (task >> 6) & 63;
-    t.t1 = (task >> 12) & 1;
-    t.t2 = (task >> 13) & 1;
-    t.Cpar = Cpar;
-    t.lg = max(0, t.l - Geo<D>::G);
-    t.cs = D * (t.l - t.lg);
-    t.npar = t.lg >= 2 ? Geo<D>::NPAR : (t.lg == 1 ? (1 << D) : 1);
-    return t;
-}
-
-// process (or queue) every batch of a task
-template <int D, int SCHEME, bool STATS>
-__device__ __forceinline__ void do_task(const SampleArgs& a, WarpSmem<D>& W, const TaskDesc& t, uint16_t task,
-                                        unsigned& fill, Counters& C)
-{
-    int nchild;
-    setup_task<D>(a, W, t, nchild);
-    for (int c0 = 0, b = 0; c0 < nchild; c0 += Geo<D>::CB, ++b) {
-        const int nc = min(Geo<D>::CB, nchild - c0);
-        unsigned long long work;
-        const unsigned long long U = setup_batch<D, SCHEME>(a, W, t, c0, nc, work);
-        if (STATS && lane_id() == 0)
-            for (int s = 0; s < nc * 3; ++s)
-                if (s % 3 && W.seq[s / 3][s % 3].units) ++C.ev2;
-        if (U == 0) continue;
-        if (work > BIG_WORK) {  // too much for one warp: queue unit ranges for k_big
-            if (lane_id() == 0) {
-                const unsigned long long per = max(1ull, U * ITEM_WORK / work);
-                const unsigned long long nit = (U + per - 1) / per;
-                const unsigned base = atomicAdd(a.nitems, (unsigned)min(nit, 0xFFFFFFFFull));
-                if ((unsigned long long)base + nit > a.items_cap) {
-                    atomicOr(a.err, ERR_ITEMS);
-                } else {
-                    for (unsigned long long k = 0; k < nit; ++k) {
-                        BigItem it;
-                        it.Cpar = t.Cpar;
-                        it.task = task;
-                        it.i = (uint8_t)t.i;
-                        it.batch = (uint8_t)b;
-                        it.lo = k * per;
-                        it.hi = min(U, (k + 1) * per);
-                        a.items[base + k] = it;
-                    }
-                }
+    if (lane_id() == 0) {
+        const unsigned long long per = max(1ull, U * a.item_work / work);
+        const unsigned long long nit = (U + per - 1) / per;
+        const unsigned base = atomicAdd(a.nitems, (unsigned)min(nit, 0xFFFFFFFFull));
+        if ((unsigned long long)base + nit > a.items_cap) {
+            atomicOr(a.err, ERR_ITEMS);
+        } else {
+            for (unsigned long long k = 0; k < nit; ++k) {
+                BigItem it;
+                it.Cpar = t.Cpar;
+                it.task = task;
+                it.i = (uint8_t)t.i;
+                it.batch = (uint8_t)batch;
+                it.lo = k * per;
+                it.hi = min(U, (k + 1) * per);
+                a.items[base + k] = it;
             }
-            __syncwarp();
-            continue;
         }
-        run_units<D, SCHEME, STATS>(a, W, t, nc, 0, U, fill, C);
     }
+    __syncwarp();
 }
 
-// persistent warps pull tiles of 32 sorted points; each point's owned tasks are processed by
-// the whole warp, one task at a time
+// ---------------------------------------------------------------------------------------
+// job sources
+// ---------------------------------------------------------------------------------------
+// k_sample: persistent warps pull tiles of 32 sorted points; each point lists the jobs it owns
 template <int D, int SCHEME, bool STATS>
-__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_sample(SampleArgs a)
-{
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
-    const Plan* pl = a.pl;
-    const unsigned lane = lane_id();
-    unsigned fill = 0;
-    Counters C = {};
-    for (;;) {
-        unsigned tile = 0;
-        if (lane == 0) tile = atomicAdd(a.tile_ctr, 1u);
-        tile = __shfl_sync(0xffffffffu, tile, 0);
-        if (tile >= a.ntiles) break;
+struct TileSource {
+    unsigned tile = 0;
+    uint32_t total = 0, tk = 0;  // jobs of the tile (warp-uniform), next one
+    int i = 0, lf = 255;         // this lane's point
+    uint32_t code = 0, cnt = 0, start = 0;
+    // pending task with further batches (d >= 4)
+    bool pend = false;
+    TaskDesc pt;
+    uint16_t ptask = 0;
+    int pbatch = 0;
+
+    __device__ __forceinline__ bool next_tile(const SampleArgs& a)
+    {
+        const Plan* pl = a.pl;
+        const unsigned lane = lane_id();
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(a.tile_ctr, 1u);
+        tile = __shfl_sync(FULL, t, 0);
+        if (tile >= a.ntiles) return false;
         const uint32_t p = tile * 32 + lane;
-        int i = 0, lf = 255;
-        uint32_t code = 0;
+        i = 0;
+        lf = 255;
+        code = 0;
         if (p < a.n) {
             int lo = 0, hi = pl->L - 1;  // layer: last with lstart <= p
             while (lo < hi) {
@@ -723,49 +639,340 @@ __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_sample(Sampl
                 lf = xr == 0 ? 255 : (int)pl->I[i] - (31 - __clz(xr)) / D;
             }
         }
-        const uint32_t cnt = lf == 255 ? 0u : pl->tcnt[i * 33 + lf];
-        uint32_t total;
-        const uint32_t start = warp_excl_scan(cnt, total);
-        for (uint32_t tk = 0; tk < total; ++tk) {
-            const unsigned own = __ballot_sync(0xffffffffu, cnt > 0 && start <= tk);
-            const int ol = 31 - __clz(own);
-            const int oi = __shfl_sync(0xffffffffu, i, ol);
-            const int olf = __shfl_sync(0xffffffffu, lf, ol);
-            const uint32_t ocode = __shfl_sync(0xffffffffu, code, ol);
-            const uint32_t ostart = __shfl_sync(0xffffffffu, start, ol);
-            GCHK(pl->toff[oi * 33 + olf] + (tk - ostart) < a.ntasks);
-            const uint16_t task = __ldg(&a.tasks[pl->toff[oi * 33 + olf] + (tk - ostart)]);
-            const int lg = max(0, ((task >> 6) & 63) - Geo<D>::G);
-            const uint32_t Cpar = ocode >> (D * ((int)pl->I[oi] - lg));
-            const TaskDesc t = make_task<D>(pl, oi, task, Cpar);
-            do_task<D, SCHEME, STATS>(a, W, t, task, fill, C);
+        cnt = lf == 255 ? 0u : pl->tcnt[i * 33 + lf];
+        start = warp_excl_scan(cnt, total);
+        tk = 0;
+        return true;
+    }
+
+    // set up the next job into S; false when the grid's tiles are exhausted
+    __device__ __forceinline__ bool next(const SampleArgs& a, Slot<D>& S, unsigned long long& lo,
+                                         unsigned long long& hi, Counters& C)
+    {
+        const Plan* pl = a.pl;
+        for (;;) {
+            TaskDesc t;
+            uint16_t task;
+            int batch;
+            if (pend) {
+                t = pt;
+                task = ptask;
+                batch = pbatch;
+            } else {
+                while (tk >= total)
+                    if (!next_tile(a)) return false;
+                const unsigned own = __ballot_sync(FULL, cnt > 0 && start <= tk);
+                const int ol = 31 - __clz(own);
+                const int oi = __shfl_sync(FULL, i, ol);
+                const int olf = __shfl_sync(FULL, lf, ol);
+                const uint32_t ocode = __shfl_sync(FULL, code, ol);
+                const uint32_t ostart = __shfl_sync(FULL, start, ol);
+                GCHK(pl->toff[oi * 33 + olf] + (tk - ostart) < a.ntasks);
+                task = __ldg(&a.tasks[pl->toff[oi * 33 + olf] + (tk - ostart)]);
+                ++tk;
+                const int lg = max(0, ((task >> 6) & 63) - Geo<D>::G);
+                t = make_task<D>(oi, task, ocode >> (D * ((int)pl->I[oi] - lg)));
+                batch = 0;
+            }
+            const JobSetup js = setup_job<D, SCHEME>(a, S, t, batch);
+            if (STATS && lane_id() == 0) C.ev2 += js.nseq2;
+            const unsigned long long U = js.U, work = js.work;
+            pend = (batch + 1) * Geo<D>::CB < js.nchild;
+            if (pend) {
+                pt = t;
+                ptask = task;
+                pbatch = batch + 1;
+            }
+            if (U == 0) continue;
+            if (work > a.big_work) {  // too much for one warp: queue unit ranges for k_big
+                push_items(a, t, task, batch, U, work);
+                continue;
+            }
+            lo = 0;
+            hi = U;
+            return true;
         }
     }
+};
+
+// k_big: warps pull queued items (unit ranges of big jobs)
+template <int D, int SCHEME, bool STATS>
+struct ItemSource {
+    unsigned k, nit, stride;
+    __device__ __forceinline__ bool next(const SampleArgs& a, Slot<D>& S, unsigned long long& lo,
+                                         unsigned long long& hi, Counters& C)
+    {
+        for (;;) {
+            if (k >= nit) return false;
+            const BigItem it = a.items[k];
+            k += stride;
+            const TaskDesc t = make_task<D>(it.i, it.task, it.Cpar);
+            setup_job<D, SCHEME>(a, S, t, it.batch);  // sequences were counted by the job that queued the item
+            (void)C;
+            if (it.hi <= it.lo) continue;
+            lo = it.lo;
+            hi = it.hi;
+            return true;
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------------------
+// the engine.  Per iteration every lane (1) computes one Philox block: the next draw of its jump
+// chain, or else the pair-keyed uniform of its pending type-I candidate; (2) advances its chain,
+// which yields the lane's NEXT candidate (a landing); (3) evaluates its PENDING candidate, whose
+// point records were loaded in the previous iteration; (4) if it holds no chain, takes a unit of
+// the dispatch slot (a type-I unit is the next candidate by itself, a chunk starts a chain);
+// (5) issues the loads of the next candidate.  The loads are in flight across the Philox and
+// the draw of the following iteration (software pipelining).  A lane never needs two Philox
+// blocks in one iteration: a pending type-I candidate implies it held no chain.  When the
+// dispatch slot runs dry, the next job is set up in a slot no lane's chain refers to.
+// ---------------------------------------------------------------------------------------
+template <int D, int SCHEME, bool STATS, class Src>
+__device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src& src, Counters& C)
+{
+    const Plan* pl = a.pl;
+    const unsigned lane = lane_id();
+    const bool T0 = pl->T == 0.0;
+    const double s_ = pl->s, invT = pl->invT;
+    const long long t_start = clock64();
+    unsigned long long n_jobs = 0, n_iter = 0, n_steps = 0;
+    unsigned fill = 0;
+    int ds = 0, dq = 0;  // dispatch slot, its first sequence with units left
+    unsigned long long dnext = 0, dhi = 0;
+    bool more = true;
+    // chain state (type-II)
+    bool chain = false;
+    int ls = 0, cc = 0, kind = 0;
+    long long pos = 0, end = 0;
+    uint32_t r = 0, ch = 0, Bev = 0, eb0 = 0, enB = 0;
+    // pending candidate: kind (-1: none), acceptance uniform and bound (type-II), loaded data
+    int pk = -1;
+    double pra = 0.0, ppbar = 1.0;
+    double xu[D], xv[D], wu = 0.0, wv = 0.0;
+    uint32_t ua = 0, ub = 0;
+#pragma unroll
+    for (int k = 0; k < D; ++k) xu[k] = xv[k] = 0.0;
+    for (;;) {
+        if (a.wprof) {
+            ++n_iter;
+            n_steps += __popc(__ballot_sync(FULL, chain || pk >= 0));
+        }
+        // ---- (1) one Philox block per lane ----
+        uint4 o = make_uint4(0u, 0u, 0u, 0u);
+        if (!T0 && (chain || pk == 0)) {
+            uint4 ctr;
+            if (chain) {
+                const Slot<D>& S = W.slot[ls];
+                const uint32_t A = S.seq[cc][kind].A;
+                ctr = SCHEME == SCHEME_MERGED ? make_uint4(A, ch, S.job.tag | ((uint32_t)(kind - 1) << 17) | (1u << 18), r)
+                                              : make_uint4(A, Bev, S.job.tag | (ch << 17), r);
+            } else {
+                ctr = make_uint4(min(ua, ub), max(ua, ub), 0u, 3u);  // type-I: keyed by the vertex pair (R17)
+            }
+            o = philox4x32_10(ctr, a.k0, a.k1);
+        }
+        // ---- (2) the chain's draw -> next candidate ----
+        int nk = -1;
+        uint32_t npa = 0, npb = 0;
+        double nra = 0.0, npbar = 1.0;
+        if (chain) {
+            const Slot<D>& S = W.slot[ls];
+            const Seq& Q = S.seq[cc][kind];
+            ++r;
+            if (STATS) ++C.draws;
+            const double pb_ = S.job.pbar[kind - 1];
+            const double rj = u53(o.x, o.y);
+            const long long remaining = end - pos - 1;
+            // skip = floor(log(1-rj)/log1p(-pbar)) (R10): fast float path, canonical double fallback
+            long long skip = 0;
+            int st = (pb_ == 1.0 || rj == 0.0) ? (remaining <= 0 ? 1 : 0)  // z = 0 exactly
+                                               : fast_jump(__dsub_rn(1.0, rj), S.job.il2[kind - 1], remaining, skip);
+            if (STATS || st < 0) {
+                const double z = pb_ == 1.0 ? 0.0 : __ddiv_rn(log(__dsub_rn(1.0, rj)), S.job.Lbar[kind - 1]);
+                const int st2 = z >= (double)remaining ? 1 : 0;
+                if (STATS) {
+                    if (st < 0) ++C.fb;
+                    else C.mm += (st != st2) || (st == 0 && skip != (long long)z);
+                }
+                st = st2;
+                skip = st2 ? 0 : (long long)z;
+            }
+            if (st) {
+                chain = false;
+            } else {
+                pos += 1 + skip;
+                if (STATS) ++C.landings;
+                nk = kind;
+                nra = u53(o.z, o.w);
+                npbar = pb_;
+                const unsigned long long g = (unsigned long long)pos;
+                if (SCHEME == SCHEME_MERGED) {
+                    uint32_t si, ti;
+                    if (Q.N <= 0xFFFFFFFFull) {
+                        si = (uint32_t)g / Q.M;
+                        ti = (uint32_t)g - si * Q.M;
+                    } else {
+                        si = (uint32_t)(g / Q.M);
+                        ti = (uint32_t)(g - (unsigned long long)si * Q.M);
+                    }
+                    uint32_t B;
+                    npa = Q.a0 + si;
+                    npb = locate<D>(S, S.job.npar, S.job.cs, cc, kind, ti, B);
+                } else {
+                    const uint32_t si = (uint32_t)(g / enB), ti = (uint32_t)(g - (unsigned long long)si * enB);
+                    npa = Q.a0 + si;
+                    npb = eb0 + ti;
+                }
+            }
+        }
+        // ---- (3) evaluate the pending candidate (records loaded last iteration) ----
+        bool edge = false;
+        if (pk >= 0) {
+            const double Dp = dist_pow<D>(xu, xv);
+            if (T0) {
+                edge = Dp <= __dmul_rn(__dmul_rn(wu, wv), s_);
+            } else {
+                // type-I: edge iff p >= 1 or r < p; type-II: edge iff r_acc * pbar < p (R14).
+                // Both are "x < p" with x < 1.
+                const double x = pk == 0 ? u53(o.x, o.y) : __dmul_rn(pra, ppbar);
+                const int fe = fast_lt_prob(x, wu, wv, s_, Dp, invT);
+                edge = fe == 1;
+                if (STATS || fe < 0) {
+                    const double p = prob_uv(wu, wv, s_, Dp, invT);
+                    const bool e2 = x < p;
+                    if (STATS) {
+                        if (fe < 0) ++C.fb;
+                        else C.mm += e2 != (fe == 1);
+                        if (pk == 0) C.nt1 += p < 1.0 && fabs(x - p) < 1e-12;
+                        else C.nt2 += fabs(x - p) < 1e-12 * ppbar;
+                    }
+                    edge = e2;
+                }
+            }
+            if (STATS) {
+                if (pk == 0) ++C.cand1;
+                if (edge) {
+                    if (pk == 0) ++C.edges1;
+                    else ++C.edges2;
+                }
+            }
+        }
+        warp_emit(a, W.ebuf, fill, edge, ua, ub);
+        // ---- (4) job setup when the dispatch slot is exhausted, then dispatch ----
+        if (dnext >= dhi && more) {
+            const unsigned occupied = __reduce_or_sync(FULL, chain ? (1u << ls) : 0u);
+            const int ns = __ffs(~occupied) - 1;
+            if (ns < Geo<D>::NSLOT) {
+                unsigned long long lo, hi;
+                if (src.next(a, W.slot[ns], lo, hi, C)) {
+                    ++n_jobs;
+                    ds = ns;
+                    dnext = lo;
+                    dhi = hi;
+                    dq = 0;
+                    while (W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
+                } else {
+                    more = false;
+                }
+            }
+        }
+        const unsigned idle = __ballot_sync(FULL, !chain);
+        if (!chain && dnext < dhi) {
+            const unsigned long long u = dnext + __popc(idle & ((1u << lane) - 1u));
+            if (u < dhi) {
+                const Slot<D>& S = W.slot[ds];
+                int q = dq;  // sequence holding unit u
+                while (S.uoff[q + 1] <= u) ++q;
+                const int qc = q / 3, qk = q - 3 * qc;
+                const Seq& Q = S.seq[qc][qk];
+                const unsigned long long x = u - S.uoff[q];
+                if (qk == 0) {
+                    uint32_t si, ti;
+                    if (x <= 0xFFFFFFFFull) {
+                        si = (uint32_t)x / Q.M;
+                        ti = (uint32_t)x - si * Q.M;
+                    } else {
+                        si = (uint32_t)(x / Q.M);
+                        ti = (uint32_t)(x - (unsigned long long)si * Q.M);
+                    }
+                    uint32_t B;
+                    npa = Q.a0 + si;
+                    npb = locate<D>(S, S.job.npar, S.job.cs, qc, 0, ti, B);
+                    if (!(S.job.same_layer && B == Q.A && npb <= npa)) nk = 0;  // same cell: only s < t (R16)
+                } else {
+                    chain = true;
+                    ls = ds;
+                    cc = qc;
+                    kind = qk;
+                    r = 0;
+                    if (SCHEME == SCHEME_MERGED) {
+                        ch = (uint32_t)x;
+                        const unsigned long long st = x << Q.cl2;
+                        pos = (long long)st - 1;
+                        end = (long long)min(Q.N, st + (1ull << Q.cl2));
+                    } else {
+                        int c2;
+                        locate_event<D>(S, S.job.clog2[qk - 1], S.job.npar, S.job.cs, qc, qk, Q.nA, (uint32_t)x, Bev,
+                                        eb0, enB, ch, c2);
+                        const unsigned long long N = (unsigned long long)Q.nA * enB;
+                        const unsigned long long st = (unsigned long long)ch << c2;
+                        pos = (long long)st - 1;
+                        end = (long long)min(N, st + (1ull << c2));
+                    }
+                    if (STATS) ++C.chunks;
+                }
+            }
+        }
+        if (dnext < dhi) {
+            dnext = min(dhi, dnext + __popc(idle));
+            if (dnext < dhi)
+                while (W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
+        }
+        // ---- (5) issue the loads of the next candidate ----
+        pk = nk;
+        pra = nra;
+        ppbar = npbar;
+        if (nk >= 0) {
+            load_rec<D>(a, npa, xu, wu);
+            load_rec<D>(a, npb, xv, wv);
+            ua = __ldg(&a.sid[npa]);
+            ub = __ldg(&a.sid[npb]);
+        }
+        if (!more && dnext >= dhi && !__any_sync(FULL, chain || pk >= 0)) break;
+    }
     warp_flush(a, W.ebuf, fill);
+    if (a.wprof && lane == 0) {
+        const unsigned w = blockIdx.x * Geo<D>::WPB + (threadIdx.x >> 5);
+        unsigned long long* op = a.wprof + 4ull * w;
+        op[0] += (unsigned long long)(clock64() - t_start);
+        op[1] += n_jobs;
+        op[2] += n_iter;
+        op[3] += n_steps;
+    }
+}
+
+template <int D, int SCHEME, bool STATS>
+__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_sample(SampleArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
+    Counters C = {};
+    TileSource<D, SCHEME, STATS> src;
+    engine<D, SCHEME, STATS>(a, W, src, C);
     flush_counters<STATS>(a, C);
 }
 
-// big items: one warp per item (rebuilds the task's batch and runs its unit range)
 template <int D, int SCHEME, bool STATS>
 __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_big(SampleArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
-    unsigned fill = 0;
     Counters C = {};
-    const unsigned nit = min(*a.nitems, a.items_cap);
-    const unsigned nw = gridDim.x * Geo<D>::WPB;
-    for (unsigned k = blockIdx.x * Geo<D>::WPB + (threadIdx.x >> 5); k < nit; k += nw) {
-        const BigItem it = a.items[k];
-        const TaskDesc t = make_task<D>(a.pl, it.i, it.task, it.Cpar);
-        int nchild;
-        setup_task<D>(a, W, t, nchild);
-        const int c0 = it.batch * Geo<D>::CB;
-        const int nc = min(Geo<D>::CB, nchild - c0);
-        unsigned long long work;
-        setup_batch<D, SCHEME>(a, W, t, c0, nc, work);
-        run_units<D, SCHEME, STATS>(a, W, t, nc, it.lo, it.hi, fill, C);
-    }
-    warp_flush(a, W.ebuf, fill);
+    ItemSource<D, SCHEME, STATS> src;
+    src.nit = min(*a.nitems, a.items_cap);
+    src.stride = gridDim.x * Geo<D>::WPB;
+    src.k = blockIdx.x * Geo<D>::WPB + (threadIdx.x >> 5);
+    engine<D, SCHEME, STATS>(a, W, src, C);
     flush_counters<STATS>(a, C);
 }

@@ -43,5 +43,7 @@ for (n, d, T, beta) in cases:
             sg, so_ = set(g.tolist()), set(o.tolist())
             extra = f" gpu-only {len(sg - so_)} oracle-only {len(so_ - sg)} dup {len(g) - len(sg)}"
         print(f"n={n} d={d} T={T} scheme={scheme}: {'OK' if ok else 'MISMATCH'} m={len(g)}/{len(o)} "
-              f"counters {'ok' if cok else cnt} gpu {1e3 * (t1 - t0):.1f} ms{extra}", flush=True)
+              f"counters {'ok' if cok else cnt} fb {st['fast_fallback']} mm {st['fast_mismatch']} "
+              f"gpu {1e3 * (t1 - t0):.1f} ms{extra}", flush=True)
+        bad += st["fast_mismatch"] != 0
 print("FAILURES", bad)
