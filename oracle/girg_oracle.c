@@ -310,6 +310,8 @@ typedef struct {
      * layer i occupies order[lstart[i] .. lstart[i+1]); P[i][C] = number of layer-i vertices
      * in cells before C at level I(i). */
     uint32_t *order;
+    uint32_t *codeI; /* Morton code at I(layer) of each sorted point (order[] positions) */
+    uint64_t *mpre, *mb0; /* R22 scratch: 6^d + 1 entries each */
     uint64_t lstart[65];
     uint32_t *P[64];
     /* type-II tables per (i, j, level, class) */
@@ -502,41 +504,51 @@ static int cmp_u32(const void *a, const void *b)
     return x < y ? -1 : x > y;
 }
 
-/* D_k(A) for both classes: out2/out3 receive the sorted cell lists, returns via n2/n3 */
-static void distant_cells(const or_ctx *c, int l, uint32_t A, int i, int j, uint32_t *out2,
-                          int *n2, uint32_t *out3, int *n3)
+/* D_2(A), D_3(A) without the i = j restriction: the children of the neighbours of parent(A) (on
+ * the torus) that are not neighbours of A, split by delta_max, each list in increasing Morton
+ * order (parents sorted by code, then their 2^d children in child-code order). */
+static void distant_cells(const or_ctx *c, int l, uint32_t A, uint32_t *out2, int *n2, uint32_t *out3,
+                          int *n3)
 {
-    int d = c->d;
-    uint32_t pa[5], q[5];
-    or_morton_decode(A >> d, d, l - 1, pa);
-    uint32_t side = 1u << (l - 1);
+    int d = c->d, np = 0;
+    uint32_t ac[5], pa[5], q[5], par[243];
+    or_morton_decode(A, d, l, ac);
+    for (int k = 0; k < d; k++) pa[k] = ac[k] >> 1;
+    uint32_t side = 1u << l, sidep = 1u << (l - 1);
     int noff = 1;
     for (int k = 0; k < d; k++) noff *= 3;
-    *n2 = 0;
-    *n3 = 0;
-    for (int o = 0; o < noff; o++) { /* parent neighbours (torus), offsets in {-1,0,1}^d */
+    for (int o = 0; o < noff; o++) { /* parent neighbours, offsets in {-1,0,1}^d */
         int r = o;
         for (int k = 0; k < d; k++) {
             int off = r % 3 - 1;
             r /= 3;
-            q[k] = (pa[k] + side + (uint32_t)off) % side;
+            q[k] = (pa[k] + sidep + (uint32_t)off) % sidep;
         }
         uint32_t P = or_morton_encode(q, d, l - 1);
+        int dup = 0; /* on levels <= 2 several offsets wrap onto the same parent */
+        for (int t = 0; t < np; t++)
+            if (par[t] == P) { dup = 1; break; }
+        if (!dup) par[np++] = P;
+    }
+    qsort(par, (size_t)np, sizeof(uint32_t), cmp_u32);
+    *n2 = 0;
+    *n3 = 0;
+    for (int t = 0; t < np; t++) {
+        or_morton_decode(par[t], d, l - 1, q);
         for (uint32_t ch = 0; ch < (1u << d); ch++) {
-            uint32_t B = (P << d) | ch;
-            if (or_are_neighbors(A, B, d, l)) continue;
-            if (i == j && B <= A) continue;
-            int dm = or_delta_max(A, B, d, l);
-            uint32_t *out = dm == 2 ? out2 : out3;
-            int *no = dm == 2 ? n2 : n3;
-            int dup = 0; /* on levels <= 2 several offsets wrap onto the same parent */
-            for (int t = 0; t < *no; t++)
-                if (out[t] == B) { dup = 1; break; }
-            if (!dup) out[(*no)++] = B;
+            uint32_t dm = 0;
+            for (int k = 0; k < d; k++) {
+                uint32_t b = 2 * q[k] + ((ch >> (d - 1 - k)) & 1u);
+                uint32_t g = b > ac[k] ? b - ac[k] : ac[k] - b;
+                if (side - g < g) g = side - g; /* torus gap */
+                if (g > dm) dm = g;
+            }
+            if (dm <= 1) continue; /* a neighbour of A (type-I or a deeper level) */
+            uint32_t B = (par[t] << d) | ch;
+            if (dm == 2) out2[(*n2)++] = B;
+            else out3[(*n3)++] = B;
         }
     }
-    qsort(out2, (size_t)*n2, sizeof(uint32_t), cmp_u32);
-    qsort(out3, (size_t)*n3, sizeof(uint32_t), cmp_u32);
 }
 
 static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, const uint32_t *Bs, int nBs)
@@ -544,9 +556,8 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
     uint64_t a0, a1;
     vrange(c, i, A, l, &a0, &a1);
     uint64_t nA = a1 - a0;
-    /* prefix of |V_j^B| over the concatenation */
-    uint64_t *pre = (uint64_t *)malloc(sizeof(uint64_t) * ((size_t)nBs + 1));
-    uint64_t *b0 = (uint64_t *)malloc(sizeof(uint64_t) * ((size_t)nBs + 1));
+    /* prefix of |V_j^B| over the concatenation (scratch owned by merged_all) */
+    uint64_t *pre = c->mpre, *b0 = c->mb0;
     pre[0] = 0;
     for (int t = 0; t < nBs; t++) {
         uint64_t lo, hi;
@@ -555,7 +566,7 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
         pre[t + 1] = pre[t] + (hi - lo);
     }
     uint64_t M = pre[nBs], N = nA * M;
-    if (N == 0) { free(pre); free(b0); return; }
+    if (N == 0) return;
     c->st->ev2_nonempty++;
     c->st->cand2 += N;
     const uint32_t *Va = c->order + c->lstart[i], *Vb = c->order + c->lstart[j];
@@ -564,12 +575,11 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
             for (int t = 0; t < nBs; t++)
                 for (uint64_t v = b0[t]; v < b0[t] + (pre[t + 1] - pre[t]); v++)
                     c->cover[(uint64_t)Va[s] * c->n + Vb[v]]++;
-        free(pre); free(b0);
         return;
     }
     size_t ti = TAB(c, i, j, l, k - 2);
     double pbar = c->pbar[ti], Lbar = c->Lbar[ti];
-    if (pbar == 0.0) { free(pre); free(b0); return; }
+    if (pbar == 0.0) return;
     int cl2 = 0;
     cl2 = 1 - ilogb(pbar);
     if (cl2 < 0) cl2 = 0;
@@ -607,8 +617,6 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
             if (ra * pbar < p) { c->st->acc2++; emit(c, u, v); }
         }
     }
-    free(pre);
-    free(b0);
 }
 
 /* shard ownership of an event whose A cell is at level l */
@@ -669,29 +677,41 @@ static void merged_all(or_ctx *c)
     for (int k = 0; k < d; k++) noff *= 6;
     uint32_t *l2 = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)noff);
     uint32_t *l3 = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)noff);
+    c->mpre = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(noff + 1));
+    c->mb0 = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(noff + 1));
     for (int l = 2; l <= c->lv.maxCL; l++)
-        for (int pr = 0; pr < c->nge[l]; pr++) {
-            int i = c->ge[l][pr][0], j = c->ge[l][pr][1];
+        for (int i = 0; i < c->lv.L; i++) {
+            int any = 0;
+            for (int pr = 0; pr < c->nge[l]; pr++) any |= c->ge[l][pr][0] == i;
+            if (!any) continue;
             int sh = d * (c->lv.I[i] - l);
-            const uint32_t *Va = c->order + c->lstart[i];
+            const uint32_t *code = c->codeI + c->lstart[i];
             uint64_t ni = c->lstart[i + 1] - c->lstart[i];
-            uint32_t prevA = 0;
             for (uint64_t s = 0; s < ni; s++) {
-                double xv[5];
-                uint32_t A = or_cell_of_point(xcoord(c, Va[s], xv), d, c->lv.I[i]) >> sh;
-                if (s > 0 && A == prevA) continue;
-                prevA = A;
+                uint32_t A = code[s] >> sh;
+                if (s > 0 && (code[s - 1] >> sh) == A) continue; /* first point of the cell */
                 uint64_t b = blk_of(c, l, A);
                 if (b < c->blo || b >= c->bhi) continue;
                 int n2, n3;
-                distant_cells(c, l, A, i, j, l2, &n2, l3, &n3);
-                c->st->ev2 += (uint64_t)(n2 + n3);
-                type2_merged(c, l, A, i, j, 2, l2, n2);
-                type2_merged(c, l, A, i, j, 3, l3, n3);
+                distant_cells(c, l, A, l2, &n2, l3, &n3);
+                for (int pr = 0; pr < c->nge[l]; pr++) {
+                    if (c->ge[l][pr][0] != i) continue;
+                    int j = c->ge[l][pr][1];
+                    int s2 = 0, s3 = 0; /* i == j: only B > A (R16); the lists are sorted */
+                    if (i == j) {
+                        while (s2 < n2 && l2[s2] <= A) s2++;
+                        while (s3 < n3 && l3[s3] <= A) s3++;
+                    }
+                    c->st->ev2 += (uint64_t)(n2 - s2 + n3 - s3);
+                    type2_merged(c, l, A, i, j, 2, l2 + s2, n2 - s2);
+                    type2_merged(c, l, A, i, j, 3, l3 + s3, n3 - s3);
+                }
             }
         }
     free(l2);
     free(l3);
+    free(c->mpre);
+    free(c->mb0);
 }
 
 /* test hook output of the Lemma-1 index */
@@ -777,6 +797,9 @@ static int or_run(const double *w, const double *x, uint64_t n, int d, double T,
             int i = lay[v];
             c->order[c->lstart[i] + cur[i][cell[v]]++] = (uint32_t)v;
         }
+        c->codeI = (uint32_t *)malloc(sizeof(uint32_t) * (n ? n : 1));
+        if (!c->codeI) { rc = OR_ENOMEM; for (int i = 0; i < L; i++) free(cur[i]); goto done; }
+        for (uint64_t s = 0; s < n; s++) c->codeI[s] = cell[c->order[s]];
         for (int i = 0; i < L; i++) free(cur[i]);
     }
 
@@ -850,7 +873,7 @@ static int or_run(const double *w, const double *x, uint64_t n, int d, double T,
     if (!rc && c->m > cap) rc = OR_ECAPACITY;
 
 done:
-    free(c->order); free(cell); free(lay);
+    free(c->order); free(c->codeI); free(cell); free(lay);
     for (int i = 0; i < 64; i++) free(c->P[i]);
     free(c->pbar); free(c->Lbar); free(c->clog2);
     free(c);

@@ -597,7 +597,7 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
     // first point of its cell; it stays first on every finer level) is <= lg.  Type-I if
     // l == CL(i,j), type-II if 2 <= l (T > 0).
     hp.tasks.clear();
-    const int G = d == 1 ? 3 : 1;
+    const int G = d == 1 ? 4 : 1;  // Geo<D>::G
     for (int i = 0; i < p.L; ++i)
         for (int lf = 0; lf <= 32; ++lf) {
             p.toff[i * 33 + lf] = (uint32_t)hp.tasks.size();
@@ -829,8 +829,8 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         a.nP = K + 1;
         a.ntab = (unsigned)hp.tab.size();
         a.ntasks = (unsigned)hp.tasks.size();
-        a.big_work = BIG_WORK;
-        a.item_work = ITEM_WORK;
+        a.big_work = big_work(d);
+        a.item_work = item_work(d);
         if (const char* e = getenv("GIRG_BIG_WORK")) a.big_work = strtoull(e, nullptr, 10);
         if (const char* e = getenv("GIRG_ITEM_WORK")) a.item_work = strtoull(e, nullptr, 10);
         a.wprof = nullptr;

@@ -44,22 +44,23 @@
 #endif
 
 constexpr int SCHEME_EVENT = 0, SCHEME_MERGED = 1;
-constexpr int EB = 256;                          // staged edges per warp
-constexpr unsigned long long BIG_WORK = 1024;    // weighted units above which a job is queued
-constexpr unsigned long long ITEM_WORK = 512;    // weighted units per queued item
+constexpr int EB = 128;                          // staged edges per warp
+// weighted units (a chunk counts 8) above which a job is queued for k_big, and per queued item
+__host__ __device__ constexpr unsigned long long big_work(int d) { return d <= 2 ? 2048ull : 8192ull; }
+__host__ __device__ constexpr unsigned long long item_work(int d) { return d <= 2 ? 1024ull : 4096ull; }
 constexpr int ERR_ITEMS = 16;
 constexpr unsigned FULL = 0xffffffffu;
 
 template <int D>
 struct Geo {
-    static constexpr int G = D == 1 ? 3 : 1;                 // levels between a task cell and its children
+    static constexpr int G = D == 1 ? 4 : 1;                 // levels between a task cell and its children
     static constexpr int NCH = 1 << (D * G);                 // children (= sub-cells per region parent)
     static constexpr int NPAR = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : 243;  // 3^d
     static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // lg = 1: all 2^d level-1 cells
     static constexpr int CB = D <= 3 ? NCH : (D == 4 ? 4 : 2);        // children per job (batch)
     static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? 4 : 2);         // warps per block
     static constexpr int MINB = D <= 2 ? 3 : (D == 3 ? 3 : 1);        // resident blocks per SM (register cap)
-    static constexpr int NSLOT = D <= 2 ? 4 : (D == 3 ? 3 : 2);       // job slots per warp (pipeline depth)
+    static constexpr int NSLOT = D == 1 ? 3 : (D <= 3 ? 3 : 2);       // job slots per warp (pipeline depth)
     static constexpr int RECW = D == 1 ? 2 : (D <= 3 ? 4 : 6);       // doubles per point record
 };
 
@@ -84,13 +85,10 @@ struct Counters {
     unsigned long long cand1, ev2, chunks, draws, landings, edges1, edges2, nt1, nt2, fb, mm;
 };
 
-// one (child, kind) sequence of a job
+// one (child, kind) sequence of a job (its unit count is the difference of the slot's uoff)
 struct Seq {
-    unsigned long long units;  // candidates (kind 0) or chunks (kinds 1, 2)
-    unsigned long long N;      // merged: nA * M
-    uint32_t A, a0, nA, M;     // child cell, its sorted range, candidates per row (kind 0 / merged)
-    int cl2;                   // log2 chunk length (merged)
-    int pad;
+    uint32_t A, a0, nA, M;  // child cell, its sorted range, candidates per row (kind 0 / merged)
+    int cl2;                // log2 chunk length (merged)
 };
 
 struct BigItem {
@@ -244,6 +242,31 @@ __device__ __forceinline__ void load_rec(const SampleArgs& a, uint32_t p, double
 #pragma unroll
     for (int k = 0; k < D; ++k) xp[k] = v[k];
     w = v[D];
+}
+
+// ---- cold paths, out of line so that the engine loop stays small in the instruction cache ----
+// canonical jump skip z = log(1-rj)/log1p(-pbar) (R10)
+__device__ __noinline__ double exact_skip(double rj, double Lbar) { return __ddiv_rn(log(__dsub_rn(1.0, rj)), Lbar); }
+// canonical p_uv (Eq. 1, kappa form)
+__device__ __noinline__ double exact_prob(double wu, double wv, double s, double Dp, double invT)
+{
+    return prob_uv(wu, wv, s, Dp, invT);
+}
+// 64-bit quotient / remainder (rare: only for sequences of >= 2^32 candidates)
+__device__ __noinline__ uint32_t divmod64(unsigned long long x, uint32_t m, uint32_t& rem)
+{
+    const unsigned long long q = x / m;
+    rem = (uint32_t)(x - q * m);
+    return (uint32_t)q;
+}
+__device__ __forceinline__ uint32_t divmod(unsigned long long x, uint32_t m, uint32_t& rem)
+{
+    if (x <= 0xFFFFFFFFull) {
+        const uint32_t q = (uint32_t)x / m;
+        rem = (uint32_t)x - q * m;
+        return q;
+    }
+    return divmod64(x, m, rem);
 }
 
 // chunk length (log2) of a type-II sequence of N candidates with table log2 length c0 and a
@@ -401,9 +424,18 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
         const uint32_t nA = S.achild[e + 1] - S.achild[e];
         uint32_t cnt[3] = {0u, 0u, 0u};
         uint32_t m[3] = {0u, 0u, 0u};
+        // d = 1: only the sub-cells within 3 cells of the child can be neighbours or distant
+        // cells with neighbouring parents; elsewhere every sub-cell of the parent may be
+        int s_lo = 0, s_hi = nsub - 1;
+        if (D == 1 && t.lg >= 2) {  // region = 3 parents of nsub cells, side >= 4 nsub: no wrap
+            const int base = (int)((((pc[0] << subl) - ac[0] + (side >> 1)) & msk)) - (int)(side >> 1);  // offset of sub 0
+            s_lo = max(0, -3 - base);
+            s_hi = min(nsub - 1, 3 - base);
+        }
 #pragma unroll
         for (int s = 0; s < NCH; ++s) {
             if (s >= nsub) break;
+            if (D == 1 && (s < s_lo || s > s_hi)) continue;
             uint32_t so[D];
             morton_decode<D>((uint32_t)s, so);
             uint32_t dm = 0, dp = 0;
@@ -448,46 +480,59 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
         }
     }
     __syncwarp();
-    // ---- phase 2: per (child, kind): prefix over parents and the sequence ----
-    unsigned long long units = 0;
-    if ((int)lane < nc * 3) {
-        const int cc = (int)lane / 3, k = (int)lane - 3 * cc;
-        uint32_t acc = 0;
-        for (int q = 0; q < t.npar; ++q) {
-            const uint32_t c = S.pre[cc][k][q];
-            S.pre[cc][k][q] = acc;
-            acc += c;
+    // ---- phase 2: per (child, kind): prefix over parents and the sequence (<= 2 per lane) ----
+    constexpr int NE = (3 * CB + 31) / 32;
+    unsigned long long units[NE];
+#pragma unroll
+    for (int h = 0; h < NE; ++h) {
+        units[h] = 0;
+        const int q3 = (int)lane + 32 * h;
+        if (q3 < nc * 3) {
+            const int cc = q3 / 3, k = q3 - 3 * cc;
+            uint32_t acc = 0;
+            for (int q = 0; q < t.npar; ++q) {
+                const uint32_t c = S.pre[cc][k][q];
+                S.pre[cc][k][q] = acc;
+                acc += c;
+            }
+            S.pre[cc][k][t.npar] = acc;
+            const int e = S.child[cc];
+            Seq& Q = S.seq[cc][k];
+            Q.A = (t.Cpar << t.cs) + (uint32_t)e;
+            Q.a0 = S.achild[e];
+            Q.nA = S.achild[e + 1] - Q.a0;
+            Q.M = acc;
+            Q.cl2 = 0;
+            if (k == 0) {
+                units[h] = (unsigned long long)Q.nA * acc;
+            } else if (SCHEME == SCHEME_EVENT) {
+                units[h] = acc;
+            } else if (acc && te[k - 1].pbar > 0.0) {
+                const unsigned long long N = (unsigned long long)Q.nA * acc;
+                Q.cl2 = chunk_log2(N, te[k - 1].clog2m, 32);
+                units[h] = ((N - 1) >> Q.cl2) + 1;
+            }
         }
-        S.pre[cc][k][t.npar] = acc;
-        const int e = S.child[cc];
-        Seq& Q = S.seq[cc][k];
-        Q.A = (t.Cpar << t.cs) + (uint32_t)e;
-        Q.a0 = S.achild[e];
-        Q.nA = S.achild[e + 1] - Q.a0;
-        Q.M = acc;
-        Q.cl2 = 0;
-        Q.N = 0;
-        if (k == 0) {
-            units = (unsigned long long)Q.nA * acc;
-        } else if (SCHEME == SCHEME_EVENT) {
-            units = acc;
-        } else if (acc && te[k - 1].pbar > 0.0) {
-            Q.N = (unsigned long long)Q.nA * acc;
-            Q.cl2 = chunk_log2(Q.N, te[k - 1].clog2m, 32);
-            units = ((Q.N - 1) >> Q.cl2) + 1;
-        }
-        Q.units = units;
     }
-    out.nseq2 = __popc(__ballot_sync(FULL, ((int)lane % 3) != 0 && units != 0));
     // ---- phase 3: unit offsets and weighted work ----
-    const unsigned long long incl = warp_incl_scan64(units);
-    if ((int)lane < nc * 3) S.uoff[lane + 1] = incl;
+    unsigned long long base = 0, wk = 0;
+    int n2 = 0;
+#pragma unroll
+    for (int h = 0; h < NE; ++h) {
+        const int q3 = (int)lane + 32 * h;
+        const bool kind0 = (q3 % 3) == 0;
+        const unsigned long long incl = warp_incl_scan64(units[h]) + base;
+        if (q3 < nc * 3) S.uoff[q3 + 1] = incl;
+        base = shfl64(incl, 31);
+        wk += units[h] * (kind0 ? 1ull : 8ull);
+        n2 += __popc(__ballot_sync(FULL, !kind0 && units[h] != 0));
+    }
     if (lane == 0) S.uoff[0] = 0;
-    unsigned long long wk = units * (((int)lane % 3) == 0 ? 1ull : 8ull);
 #pragma unroll
     for (int o = 16; o; o >>= 1) wk += __shfl_xor_sync(FULL, wk, o);
     out.work = wk;
-    out.U = shfl64(incl, nc * 3 - 1);
+    out.U = base;
+    out.nseq2 = n2;
     __syncwarp();
     return out;
 }
@@ -646,7 +691,7 @@ struct TileSource {
     }
 
     // set up the next job into S; false when the grid's tiles are exhausted
-    __device__ __forceinline__ bool next(const SampleArgs& a, Slot<D>& S, unsigned long long& lo,
+    __device__ __noinline__ bool next(const SampleArgs& a, Slot<D>& S, unsigned long long& lo,
                                          unsigned long long& hi, Counters& C)
     {
         const Plan* pl = a.pl;
@@ -699,7 +744,7 @@ struct TileSource {
 template <int D, int SCHEME, bool STATS>
 struct ItemSource {
     unsigned k, nit, stride;
-    __device__ __forceinline__ bool next(const SampleArgs& a, Slot<D>& S, unsigned long long& lo,
+    __device__ __noinline__ bool next(const SampleArgs& a, Slot<D>& S, unsigned long long& lo,
                                          unsigned long long& hi, Counters& C)
     {
         for (;;) {
@@ -789,7 +834,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
             int st = (pb_ == 1.0 || rj == 0.0) ? (remaining <= 0 ? 1 : 0)  // z = 0 exactly
                                                : fast_jump(__dsub_rn(1.0, rj), S.job.il2[kind - 1], remaining, skip);
             if (STATS || st < 0) {
-                const double z = pb_ == 1.0 ? 0.0 : __ddiv_rn(log(__dsub_rn(1.0, rj)), S.job.Lbar[kind - 1]);
+                const double z = pb_ == 1.0 ? 0.0 : exact_skip(rj, S.job.Lbar[kind - 1]);
                 const int st2 = z >= (double)remaining ? 1 : 0;
                 if (STATS) {
                     if (st < 0) ++C.fb;
@@ -808,19 +853,14 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 npbar = pb_;
                 const unsigned long long g = (unsigned long long)pos;
                 if (SCHEME == SCHEME_MERGED) {
-                    uint32_t si, ti;
-                    if (Q.N <= 0xFFFFFFFFull) {
-                        si = (uint32_t)g / Q.M;
-                        ti = (uint32_t)g - si * Q.M;
-                    } else {
-                        si = (uint32_t)(g / Q.M);
-                        ti = (uint32_t)(g - (unsigned long long)si * Q.M);
-                    }
+                    uint32_t ti;
+                    const uint32_t si = divmod(g, Q.M, ti);
                     uint32_t B;
                     npa = Q.a0 + si;
                     npb = locate<D>(S, S.job.npar, S.job.cs, cc, kind, ti, B);
                 } else {
-                    const uint32_t si = (uint32_t)(g / enB), ti = (uint32_t)(g - (unsigned long long)si * enB);
+                    uint32_t ti;
+                    const uint32_t si = divmod(g, enB, ti);
                     npa = Q.a0 + si;
                     npb = eb0 + ti;
                 }
@@ -839,7 +879,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 const int fe = fast_lt_prob(x, wu, wv, s_, Dp, invT);
                 edge = fe == 1;
                 if (STATS || fe < 0) {
-                    const double p = prob_uv(wu, wv, s_, Dp, invT);
+                    const double p = exact_prob(wu, wv, s_, Dp, invT);
                     const bool e2 = x < p;
                     if (STATS) {
                         if (fe < 0) ++C.fb;
@@ -888,14 +928,8 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 const Seq& Q = S.seq[qc][qk];
                 const unsigned long long x = u - S.uoff[q];
                 if (qk == 0) {
-                    uint32_t si, ti;
-                    if (x <= 0xFFFFFFFFull) {
-                        si = (uint32_t)x / Q.M;
-                        ti = (uint32_t)x - si * Q.M;
-                    } else {
-                        si = (uint32_t)(x / Q.M);
-                        ti = (uint32_t)(x - (unsigned long long)si * Q.M);
-                    }
+                    uint32_t ti;
+                    const uint32_t si = divmod(x, Q.M, ti);
                     uint32_t B;
                     npa = Q.a0 + si;
                     npb = locate<D>(S, S.job.npar, S.job.cs, qc, 0, ti, B);
@@ -910,7 +944,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                         ch = (uint32_t)x;
                         const unsigned long long st = x << Q.cl2;
                         pos = (long long)st - 1;
-                        end = (long long)min(Q.N, st + (1ull << Q.cl2));
+                        end = (long long)min((unsigned long long)Q.nA * Q.M, st + (1ull << Q.cl2));
                     } else {
                         int c2;
                         locate_event<D>(S, S.job.clog2[qk - 1], S.job.npar, S.job.cs, qc, qk, Q.nA, (uint32_t)x, Bev,
