@@ -462,12 +462,13 @@ static void type2(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
             double rj = or_u53(o[0], o[1]), ra = or_u53(o[2], o[3]);
             double z = pbar == 1.0 ? 0.0 : log(1.0 - rj) / Lbar;
             int64_t remaining = (int64_t)end - pos - 1;
-            /* jump near-tie (R10): floor(z) is an integer decided in double.  Another libm's
-             * log differs by <= 2 ulp, so z moves by < 7e-16 |z|; only a z within 1e-14 |z| of
-             * an integer, and small enough to matter (z < remaining + 1), is counted. */
+            /* jump near-tie (R21): floor(z) is an integer decided in double.  glibc's and CUDA's
+             * log are each within 1 ulp of log(1-rj), the division is correctly rounded, so the
+             * two z differ by < 3 ulp < 7e-16 |z|; only a z within 1e-15 |z| of an integer, and
+             * small enough to matter (z < remaining + 1), is counted. */
             if (z < (double)remaining + 1.0 && pbar < 1.0) {
                 double az = fabs(z);
-                if (fabs(z - nearbyint(z)) < 1e-14 * (az > 1.0 ? az : 1.0)) c->st->nt2jump++;
+                if (fabs(z - nearbyint(z)) < 1e-15 * (az > 1.0 ? az : 1.0)) c->st->nt2jump++;
             }
             if (z >= (double)remaining) break;
             pos += 1 + (int64_t)z;
@@ -602,7 +603,7 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
             int64_t remaining = (int64_t)end - pos - 1;
             if (z < (double)remaining + 1.0 && pbar < 1.0) { /* jump near-tie, as in type2 */
                 double az = fabs(z);
-                if (fabs(z - nearbyint(z)) < 1e-14 * (az > 1.0 ? az : 1.0)) c->st->nt2jump++;
+                if (fabs(z - nearbyint(z)) < 1e-15 * (az > 1.0 ? az : 1.0)) c->st->nt2jump++;
             }
             if (z >= (double)remaining) break;
             pos += 1 + (int64_t)z;
