@@ -550,8 +550,7 @@ __device__ __forceinline__ uint32_t locate(const Slot<D>& S, int npar, int cs, i
     }
     uint32_t r = t - S.pre[cc][k][lo];
     uint32_t m = S.mask[cc][k][lo];
-    for (;;) {
-        GCHK(m != 0);
+    while (m) {
         const int s = __ffs(m) - 1;
         const uint32_t nB = S.rstart[lo][s + 1] - S.rstart[lo][s];
         if (r < nB) {
@@ -561,6 +560,9 @@ __device__ __forceinline__ uint32_t locate(const Slot<D>& S, int npar, int cs, i
         r -= nB;
         m &= m - 1u;
     }
+    GCHK(false);  // unreachable: the prefix counts are sums over the mask (setup_job)
+    B = 0;
+    return S.rstart[lo][0];
 }
 
 // EVENT scheme: chunk index u of sequence (cc, k) -> event (B, its range) and chunk within it
@@ -577,8 +579,9 @@ __device__ __forceinline__ void locate_event(const Slot<D>& S, int clog2, int np
     }
     uint32_t r = u - S.pre[cc][k][lo];
     uint32_t m = S.mask[cc][k][lo];
-    for (;;) {
-        GCHK(m != 0);
+    B = b0 = nB = ch = 0;
+    cl2 = 0;
+    while (m) {
         const int s = __ffs(m) - 1;
         m &= m - 1u;
         const uint32_t nb = S.rstart[lo][s + 1] - S.rstart[lo][s];
@@ -596,6 +599,7 @@ __device__ __forceinline__ void locate_event(const Slot<D>& S, int clog2, int np
         }
         r -= nch;
     }
+    GCHK(false);  // unreachable (setup_job counted these chunks); nB = 0 makes an empty chain
 }
 
 template <bool STATS>
@@ -752,8 +756,17 @@ struct ItemSource {
             const BigItem it = a.items[k];
             k += stride;
             const TaskDesc t = make_task<D>(it.i, it.task, it.Cpar);
-            setup_job<D, SCHEME>(a, S, t, it.batch);  // sequences were counted by the job that queued the item
+            const JobSetup js = setup_job<D, SCHEME>(a, S, t, it.batch);  // sequences were counted by the job that queued it
             (void)C;
+#ifdef GIRG_DEBUG
+            if (js.U < it.hi && lane_id() == 0)
+                printf("k_big item %u: job U %llu < item hi %llu (i %d task %x Cpar %u batch %d nchild %d)\n", k - stride,
+                       js.U, it.hi, it.i, it.task, it.Cpar, it.batch, js.nchild);
+#endif
+            if (js.U < it.hi) {
+                atomicOr(a.err, ERR_ITEMS);
+                continue;
+            }
             if (it.hi <= it.lo) continue;
             lo = it.lo;
             hi = it.hi;
@@ -911,7 +924,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                     dnext = lo;
                     dhi = hi;
                     dq = 0;
-                    while (W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
+                    while (dq < 3 * Geo<D>::CB - 1 && W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
                 } else {
                     more = false;
                 }
@@ -923,7 +936,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
             if (u < dhi) {
                 const Slot<D>& S = W.slot[ds];
                 int q = dq;  // sequence holding unit u
-                while (S.uoff[q + 1] <= u) ++q;
+                while (q < 3 * Geo<D>::CB - 1 && S.uoff[q + 1] <= u) ++q;
                 const int qc = q / 3, qk = q - 3 * qc;
                 const Seq& Q = S.seq[qc][qk];
                 const unsigned long long x = u - S.uoff[q];
@@ -961,7 +974,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         if (dnext < dhi) {
             dnext = min(dhi, dnext + __popc(idle));
             if (dnext < dhi)
-                while (W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
+                while (dq < 3 * Geo<D>::CB - 1 && W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
         }
         // ---- (5) issue the loads of the next candidate ----
         pk = nk;
@@ -1004,7 +1017,9 @@ __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_big(SampleAr
     WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
     Counters C = {};
     ItemSource<D, SCHEME, STATS> src;
-    src.nit = min(*a.nitems, a.items_cap);
+    // an overflowing push skipped its whole reservation, so [0, cap) may hold unwritten items:
+    // on overflow do nothing (the host grows the queue and re-runs the sampler)
+    src.nit = (*a.err & ERR_ITEMS) ? 0u : min(*a.nitems, a.items_cap);
     src.stride = gridDim.x * Geo<D>::WPB;
     src.k = blockIdx.x * Geo<D>::WPB + (threadIdx.x >> 5);
     engine<D, SCHEME, STATS>(a, W, src, C);
