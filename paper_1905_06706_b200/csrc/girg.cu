@@ -597,7 +597,7 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
     // first point of its cell; it stays first on every finer level) is <= lg.  Type-I if
     // l == CL(i,j), type-II if 2 <= l (T > 0).
     hp.tasks.clear();
-    const int G = d == 1 ? 4 : 1;  // Geo<D>::G
+    const int G = d == 1 ? GIRG_G1 : 1;  // Geo<D>::G
     for (int i = 0; i < p.L; ++i)
         for (int lf = 0; lf <= 32; ++lf) {
             p.toff[i * 33 + lf] = (uint32_t)hp.tasks.size();
@@ -823,7 +823,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         a.nitems = (unsigned int*)(misc + 28);
         a.stats = stats_out ? d_cnt : nullptr;
         a.err = d_err;
-        unsigned int items_cap = std::max<unsigned int>(1u << 16, n32 / 4);
+        unsigned int items_cap = std::max<unsigned int>(1u << 18, n32 / 2);
         a.items = S.alloc<BigItem>(items_cap);
         a.items_cap = items_cap;
         a.nP = K + 1;
@@ -834,6 +834,8 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         if (const char* e = getenv("GIRG_BIG_WORK")) a.big_work = strtoull(e, nullptr, 10);
         if (const char* e = getenv("GIRG_ITEM_WORK")) a.item_work = strtoull(e, nullptr, 10);
         a.wprof = nullptr;
+        a.dev_flags = 0;
+        if (const char* e = getenv("GIRG_DEV_FLAGS")) a.dev_flags = (unsigned)atoi(e);
         PE.record(2, st);
         char hmisc[256];
         for (int attempt = 0;; ++attempt) {

@@ -46,21 +46,33 @@
 constexpr int SCHEME_EVENT = 0, SCHEME_MERGED = 1;
 constexpr int EB = 128;                          // staged edges per warp
 // weighted units (a chunk counts 8) above which a job is queued for k_big, and per queued item
-__host__ __device__ constexpr unsigned long long big_work(int d) { return d <= 2 ? 2048ull : 8192ull; }
-__host__ __device__ constexpr unsigned long long item_work(int d) { return d <= 2 ? 1024ull : 4096ull; }
+__host__ __device__ constexpr unsigned long long big_work(int d) { return d == 1 ? 512ull : (d == 2 ? 2048ull : 32768ull); }
+__host__ __device__ constexpr unsigned long long item_work(int d) { return d == 1 ? 256ull : (d == 2 ? 1024ull : 16384ull); }
 constexpr int ERR_ITEMS = 16;
 constexpr unsigned FULL = 0xffffffffu;
 
+#ifndef GIRG_G1
+#define GIRG_G1 3  // d = 1 task height (development knob)
+#endif
+#ifndef GIRG_NSLOT1
+#define GIRG_NSLOT1 4
+#endif
+#ifndef GIRG_NSLOT3
+#define GIRG_NSLOT3 2  // d = 3 job slots (development knob)
+#endif
+#ifndef GIRG_MINB3
+#define GIRG_MINB3 4   // d = 3 resident blocks per SM (register cap)
+#endif
 template <int D>
 struct Geo {
-    static constexpr int G = D == 1 ? 4 : 1;                 // levels between a task cell and its children
+    static constexpr int G = D == 1 ? GIRG_G1 : 1;          // levels between a task cell and its children
     static constexpr int NCH = 1 << (D * G);                 // children (= sub-cells per region parent)
     static constexpr int NPAR = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : 243;  // 3^d
     static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // lg = 1: all 2^d level-1 cells
     static constexpr int CB = D <= 3 ? NCH : (D == 4 ? 4 : 2);        // children per job (batch)
     static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? 4 : 2);         // warps per block
-    static constexpr int MINB = D <= 2 ? 3 : (D == 3 ? 3 : 1);        // resident blocks per SM (register cap)
-    static constexpr int NSLOT = D == 1 ? 3 : (D <= 3 ? 3 : 2);       // job slots per warp (pipeline depth)
+    static constexpr int MINB = D <= 2 ? 3 : (D == 3 ? GIRG_MINB3 : 1);  // resident blocks per SM (register cap)
+    static constexpr int NSLOT = D == 1 ? GIRG_NSLOT1 : (D == 2 ? 3 : (D == 3 ? GIRG_NSLOT3 : 2));  // job slots per warp
     static constexpr int RECW = D == 1 ? 2 : (D <= 3 ? 4 : 6);       // doubles per point record
 };
 
@@ -121,6 +133,7 @@ struct SampleArgs {
     unsigned int ntab, ntasks;
     unsigned long long big_work, item_work;  // job split thresholds (BIG_WORK / ITEM_WORK by default)
     unsigned long long* wprof;               // optional per-warp profile: cycles, jobs, iterations, lane steps
+    unsigned dev_flags;                      // development: 1 = set up jobs but skip their units
 };
 
 struct TaskDesc {
@@ -356,9 +369,10 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
         const int shj = D * ((int)pl->I[t.j] - t.l), shi = D * ((int)pl->I[t.i] - t.l);
         const uint32_t bj = pl->base[t.j], bi = pl->base[t.i];
         const int per = nsub + 1;
+        constexpr int PER1 = Geo<D>::NCH + 1;  // per when l >= lg + G (the common case): a constant divisor
         for (int e = lane; e < t.npar * per + per; e += 32) {
             if (e < t.npar * per) {
-                const int q = e / per, k = e - q * per;
+                const int q = per == PER1 ? e / PER1 : e / per, k = e - q * per;
                 const unsigned long long cell = ((unsigned long long)S.par[q] << t.cs) + (unsigned)k;
                 GCHK(bj + (cell << shj) < a.nP);
                 S.rstart[q][k] = __ldg(&a.P[bj + (cell << shj)]);
@@ -414,6 +428,64 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
     const uint32_t side = 1u << t.l, msk = side - 1u;
     const uint32_t side2 = side >> 1, msk2 = side2 - 1u;  // level l-1 (parent check, G > 1)
     const bool pcheck = Geo<D>::G > 1 && t.l >= 3;
+    if constexpr (Geo<D>::G == 1 && D <= 3) {
+        if (t.l >= 1) {  // sub-cells = the 2^d children of each region parent: separable per dimension
+            for (int idx = lane; idx < nc * t.npar; idx += 32) {
+                const int cc = idx / t.npar, q = idx - cc * t.npar;
+                const int e = S.child[cc];
+                const uint32_t A = (t.Cpar << D) + (uint32_t)e, P = S.par[q];
+                uint32_t ac[D], pc[D], g0[D], g1[D];
+                morton_decode<D>(A, ac);
+                morton_decode<D>(P, pc);
+#pragma unroll
+                for (int k = 0; k < D; ++k) {  // torus gaps of the two children per dimension
+                    const uint32_t d0 = ((pc[k] << 1) - ac[k]) & msk, d1 = ((pc[k] << 1) + 1u - ac[k]) & msk;
+                    g0[k] = min(d0, side - d0);
+                    g1[k] = min(d1, side - d1);
+                }
+                const int pcmp = P < t.Cpar ? -1 : (P > t.Cpar ? 1 : 0);  // Morton order of B vs A
+                const uint32_t nA = S.achild[e + 1] - S.achild[e];
+                uint32_t rs[NCH + 1];
+#pragma unroll
+                for (int k = 0; k <= NCH; ++k) rs[k] = S.rstart[q][k];
+                uint32_t cnt[3] = {0u, 0u, 0u}, m[3] = {0u, 0u, 0u};
+#pragma unroll
+                for (int sc = 0; sc < NCH; ++sc) {
+                    uint32_t dm = 0;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) dm = max(dm, ((sc >> (D - 1 - k)) & 1) ? g1[k] : g0[k]);
+                    const bool ge = pcmp > 0 || (pcmp == 0 && sc >= e), gt = pcmp > 0 || (pcmp == 0 && sc > e);
+                    int kind = -1;
+                    if (dm <= 1) {
+                        if (t.t1 && (t.i < t.j || ge)) kind = 0;
+                    } else if (t.t2 && (t.i < t.j || gt)) {
+                        kind = (int)dm - 1;
+                    }
+                    const uint32_t nB = rs[sc + 1] - rs[sc];
+                    uint32_t add = nB;
+                    if (SCHEME == SCHEME_EVENT && kind > 0) {
+                        add = 0;
+                        if (nB && te[kind - 1].pbar > 0.0) {
+                            const unsigned long long N = (unsigned long long)nA * nB;
+                            add = (uint32_t)(((N - 1) >> chunk_log2(N, te[kind - 1].clog2, 15)) + 1);
+                        }
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < 3; ++kk)
+                        if (kk == kind) {
+                            m[kk] |= 1u << sc;
+                            cnt[kk] += add;
+                        }
+                }
+#pragma unroll
+                for (int kk = 0; kk < 3; ++kk) {
+                    S.mask[cc][kk][q] = (MaskT)m[kk];
+                    S.pre[cc][kk][q] = cnt[kk];
+                }
+            }
+            goto classified;
+        }
+    }
     for (int idx = lane; idx < nc * t.npar; idx += 32) {
         const int cc = idx / t.npar, q = idx - cc * t.npar;
         const int e = S.child[cc];
@@ -479,6 +551,7 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
             S.pre[cc][kk][q] = cnt[kk];
         }
     }
+classified:
     __syncwarp();
     // ---- phase 2: per (child, kind): prefix over parents and the sequence (<= 2 per lane) ----
     constexpr int NE = (3 * CB + 31) / 32;
@@ -921,6 +994,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 if (src.next(a, W.slot[ns], lo, hi, C)) {
                     ++n_jobs;
                     ds = ns;
+                    if (a.dev_flags & 1) lo = hi;
                     dnext = lo;
                     dhi = hi;
                     dq = 0;
