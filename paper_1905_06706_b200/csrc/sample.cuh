@@ -879,6 +879,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
     uint32_t r = 0, ch = 0, Bev = 0, eb0 = 0, enB = 0;
     // pending candidate: kind (-1: none), acceptance uniform and bound (type-II), loaded data
     int pk = -1;
+    uint32_t ppa = 0, ppb = 0;
     double pra = 0.0, ppbar = 1.0;
     double xu[D], xv[D], wu = 0.0, wv = 0.0;
     uint32_t ua = 0, ub = 0;
@@ -983,6 +984,10 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                     else ++C.edges2;
                 }
             }
+            if (edge && pk > 0) {  // type-II: ids only for accepted landings (~5 %)
+                ua = __ldg(&a.sid[ppa]);
+                ub = __ldg(&a.sid[ppb]);
+            }
         }
         warp_emit(a, W.ebuf, fill, edge, ua, ub);
         // ---- (4) job setup when the dispatch slot is exhausted, then dispatch ----
@@ -1052,13 +1057,17 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         }
         // ---- (5) issue the loads of the next candidate ----
         pk = nk;
+        ppa = npa;
+        ppb = npb;
         pra = nra;
         ppbar = npbar;
         if (nk >= 0) {
             load_rec<D>(a, npa, xu, wu);
             load_rec<D>(a, npb, xv, wv);
-            ua = __ldg(&a.sid[npa]);
-            ub = __ldg(&a.sid[npb]);
+            if (nk == 0) {  // type-I: the ids key the pair's uniform (R17)
+                ua = __ldg(&a.sid[npa]);
+                ub = __ldg(&a.sid[npb]);
+            }
         }
         if (!more && dnext >= dhi && !__any_sync(FULL, chain || pk >= 0)) break;
     }
