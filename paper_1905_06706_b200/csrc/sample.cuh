@@ -26,6 +26,7 @@
 //   * jobs with too much work are split into unit-range items of a global queue (k_big).
 //   * edges are staged per warp in shared memory and written with one atomic per flush.
 #pragma once
+#include <type_traits>
 
 // GIRG_DEBUG builds (libgirg_debug.so) bounds-check the indexed accesses of the sampler
 #ifdef GIRG_DEBUG
@@ -52,10 +53,10 @@ constexpr int ERR_ITEMS = 16;
 constexpr unsigned FULL = 0xffffffffu;
 
 #ifndef GIRG_G1
-#define GIRG_G1 3  // d = 1 task height (development knob)
+#define GIRG_G1 4  // d = 1 task height (development knob)
 #endif
 #ifndef GIRG_NSLOT1
-#define GIRG_NSLOT1 4
+#define GIRG_NSLOT1 3
 #endif
 #ifndef GIRG_NSLOT3
 #define GIRG_NSLOT3 2  // d = 3 job slots (development knob)
@@ -71,7 +72,7 @@ struct Geo {
     static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // lg = 1: all 2^d level-1 cells
     static constexpr int CB = D <= 3 ? NCH : (D == 4 ? 4 : 2);        // children per job (batch)
     static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? 4 : 2);         // warps per block
-    static constexpr int MINB = D <= 2 ? 3 : (D == 3 ? GIRG_MINB3 : 1);  // resident blocks per SM (register cap)
+    static constexpr int MINB = D == 1 ? 2 : (D == 2 ? 3 : (D == 3 ? GIRG_MINB3 : 1));  // resident blocks per SM
     static constexpr int NSLOT = D == 1 ? GIRG_NSLOT1 : (D == 2 ? 3 : (D == 3 ? GIRG_NSLOT3 : 2));  // job slots per warp
     static constexpr int RECW = D == 1 ? 2 : (D <= 3 ? 4 : 6);       // doubles per point record
 };
@@ -166,9 +167,30 @@ struct Slot {
     uint8_t child[NCH];  // nonempty owned children of Cg
 };
 
+// d = 1 job slot (lane per child): each child's sequences are <= 3 cell ranges per kind
+// (neighbours a-1..a+1; distant a-2, a+2; the one of a-3, a+3 whose parent neighbours A's), kept
+// explicitly in Morton (= coordinate) order instead of per-parent masks and prefix counts.
+struct Slot1 {
+    static constexpr int NPAR = 3, NCH = Geo<1>::NCH, CB = Geo<1>::CB;
+    uint32_t par[NPAR];
+    uint32_t rstart[NPAR][NCH + 1];
+    uint32_t achild[NCH + 1];
+    uint32_t rs[CB][3][3];  // range starts (sorted positions in layer j)
+    uint32_t rn[CB][3][3];  // range lengths
+    uint32_t rc[CB][3][4];  // cumulative units before each range (candidates; EVENT type-II: chunks)
+    uint32_t rb[CB][3][3];  // cell codes
+    Seq seq[CB][3];
+    unsigned long long uoff[CB * 3 + 1];
+    JobInfo job;
+    uint8_t child[NCH];
+};
+
+template <int D>
+using SlotT = typename std::conditional<D == 1, Slot1, Slot<D>>::type;
+
 template <int D>
 struct WarpSmem {
-    Slot<D> slot[Geo<D>::NSLOT];
+    SlotT<D> slot[Geo<D>::NSLOT];
     uint2 ebuf[EB];
 };
 
@@ -318,12 +340,14 @@ struct JobSetup {
     int nseq2;                // nonempty type-II sequences (counter)
 };
 
-template <int D, int SCHEME>
-__device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, const TaskDesc t, int batch)
+// ---- job setup, common part (warp-collective): region parents in Morton order, the Lemma-1
+// ranges of their sub-cells (layer j) and of the task cell's children (layer i), the nonempty
+// owned children of this batch, the job constants.  Returns the batch's child count.
+template <int D, class SL>
+__device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const TaskDesc& t, int batch, JobSetup& out,
+                                            const TabEntry*& te)
 {
-    JobSetup out = {0ull, 0ull, 0, 0};
-    constexpr int NCH = Geo<D>::NCH, CB = Geo<D>::CB;
-    using MaskT = typename Slot<D>::MaskT;
+    constexpr int CB = SL::CB;
     const Plan* pl = a.pl;
     const unsigned lane = lane_id();
     const int nsub = 1 << t.cs;
@@ -406,8 +430,8 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
         out.nchild = cnt;
     }
     const int nc = min(CB, out.nchild - batch * CB);
-    if (nc <= 0) return out;
-    const TabEntry* te = t.t2 ? a.tab + (pl->tab_off[t.i * MAXL + t.j] + 2u * (uint32_t)(t.l - 2)) : nullptr;
+    if (nc <= 0) return 0;
+    te = t.t2 ? a.tab + (pl->tab_off[t.i * MAXL + t.j] + 2u * (uint32_t)(t.l - 2)) : nullptr;
     if (lane == 0) {
         JobInfo& J = S.job;
         J.tag = (uint32_t)t.l | ((uint32_t)t.i << 5) | ((uint32_t)t.j << 11);
@@ -423,6 +447,21 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
         }
     }
     __syncwarp();
+    return nc;
+}
+
+template <int D, int SCHEME>
+__device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, const TaskDesc t, int batch)
+{
+    JobSetup out = {0ull, 0ull, 0, 0};
+    constexpr int NCH = Geo<D>::NCH, CB = Geo<D>::CB;
+    using MaskT = typename Slot<D>::MaskT;
+    const Plan* pl = a.pl;
+    const unsigned lane = lane_id();
+    const int nsub = 1 << t.cs;
+    const TabEntry* te = nullptr;
+    const int nc = setup_common<D>(a, S, t, batch, out, te);
+    if (nc <= 0) return out;
     // ---- phase 1: classify every (child, region parent) pair in parallel ----
     const int subl = t.cs / D;  // levels between a region parent and its sub-cells
     const uint32_t side = 1u << t.l, msk = side - 1u;
@@ -610,6 +649,156 @@ classified:
     return out;
 }
 
+// d = 1 job setup: one lane per child lists its <= 3 cell ranges per kind directly (offsets
+// -3..3 from the child, or every region cell when the region is the whole level, lg <= 1).
+template <int SCHEME>
+__device__ __noinline__ JobSetup setup_job1(const SampleArgs& a, Slot1& S, const TaskDesc t, int batch)
+{
+    JobSetup out = {0ull, 0ull, 0, 0};
+    const TabEntry* te = nullptr;
+    const int nc = setup_common<1>(a, S, t, batch, out, te);
+    if (nc <= 0) return out;
+    const unsigned lane = lane_id();
+    const int subl = t.cs, nsub = 1 << t.cs;  // d = 1: the shift is the level difference
+    const uint32_t side = 1u << t.l, msk = side - 1u, side2 = side >> 1, msk2 = side2 - 1u;
+    unsigned long long units[3] = {0ull, 0ull, 0ull};
+    if ((int)lane < nc) {
+        const int cc = (int)lane, e = S.child[cc];
+        const uint32_t A = (t.Cpar << subl) + (uint32_t)e;
+        const uint32_t a0 = S.achild[e], nA = S.achild[e + 1] - a0;
+        uint32_t cb[3][3], cst[3][3], cn[3][3];
+        int nk[3] = {0, 0, 0};
+        const bool near = t.lg >= 2;  // l = lg + G >= 6: offsets -3..3 are distinct and inside the region
+        const int ncand = near ? 7 : t.npar * nsub;
+        for (int c = 0; c < ncand; ++c) {
+            uint32_t B;
+            int q, kk;
+            if (near) {
+                B = (A + (uint32_t)(c - 3)) & msk;
+                const uint32_t pb = B >> subl;
+                q = pb == S.par[0] ? 0 : (pb == S.par[1] ? 1 : 2);
+                kk = (int)(B & (uint32_t)(nsub - 1));
+            } else {
+                q = c / nsub;
+                kk = c - q * nsub;
+                B = (S.par[q] << subl) + (uint32_t)kk;
+            }
+            const uint32_t df = (B - A) & msk, dm = min(df, side - df);
+            int kind = -1;
+            if (dm <= 1) {
+                if (t.t1 && (t.i < t.j || B >= A)) kind = 0;
+            } else if (t.t2 && (t.i < t.j || B > A)) {
+                bool pn = true;  // parents neighbours (the region may hold farther cells)
+                if (t.l >= 3) {
+                    const uint32_t d2 = ((B >> 1) - (A >> 1)) & msk2;
+                    pn = min(d2, side2 - d2) <= 1;
+                }
+                if (pn) kind = (int)dm - 1;
+            }
+            if (kind < 0) continue;
+            // insert by cell code (Morton order = coordinate order in d = 1)
+            int m = nk[kind]++;
+            const uint32_t st = S.rstart[q][kk], n = S.rstart[q][kk + 1] - st;
+            while (m > 0 && cb[kind][m - 1] > B) {
+                cb[kind][m] = cb[kind][m - 1];
+                cst[kind][m] = cst[kind][m - 1];
+                cn[kind][m] = cn[kind][m - 1];
+                --m;
+            }
+            cb[kind][m] = B;
+            cst[kind][m] = st;
+            cn[kind][m] = n;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            uint32_t acc = 0;
+            const TabEntry* tk = (k > 0 && t.t2) ? &te[k - 1] : nullptr;
+            for (int r = 0; r < nk[k]; ++r) {
+                S.rs[cc][k][r] = cst[k][r];
+                S.rn[cc][k][r] = cn[k][r];
+                S.rb[cc][k][r] = cb[k][r];
+                S.rc[cc][k][r] = acc;
+                if (k == 0 || SCHEME == SCHEME_MERGED) {
+                    acc += cn[k][r];
+                } else if (cn[k][r] && tk->pbar > 0.0) {  // EVENT: chunks of the event (A, B)
+                    const unsigned long long N = (unsigned long long)nA * cn[k][r];
+                    acc += (uint32_t)(((N - 1) >> chunk_log2(N, tk->clog2, 15)) + 1);
+                }
+            }
+            S.rc[cc][k][nk[k]] = acc;
+            Seq& Q = S.seq[cc][k];
+            Q.A = A;
+            Q.a0 = a0;
+            Q.nA = nA;
+            Q.M = acc;
+            Q.cl2 = nk[k];  // merged chunk log2 set below; EVENT / type-I: unused
+            if (k == 0) {
+                units[k] = (unsigned long long)nA * acc;
+            } else if (SCHEME == SCHEME_EVENT) {
+                units[k] = acc;
+            } else {
+                Q.cl2 = 0;
+                if (acc && tk->pbar > 0.0) {
+                    const unsigned long long N = (unsigned long long)nA * acc;
+                    Q.cl2 = chunk_log2(N, tk->clog2m, 32);
+                    units[k] = ((N - 1) >> Q.cl2) + 1;
+                }
+            }
+        }
+    }
+    // unit offsets, sequence order (child, kind): lane cc's three sequences are consecutive
+    const unsigned long long mine = units[0] + units[1] + units[2];
+    const unsigned long long incl = warp_incl_scan64(mine);
+    if ((int)lane < nc) {
+        S.uoff[3 * lane + 1] = incl - mine + units[0];
+        S.uoff[3 * lane + 2] = incl - mine + units[0] + units[1];
+        S.uoff[3 * lane + 3] = incl;
+    }
+    if (lane == 0) S.uoff[0] = 0;
+    unsigned long long wk = units[0] + 8ull * (units[1] + units[2]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wk += __shfl_xor_sync(FULL, wk, o);
+    out.work = wk;
+    out.U = shfl64(incl, 31);
+    out.nseq2 = __popc(__ballot_sync(FULL, units[1] != 0)) + __popc(__ballot_sync(FULL, units[2] != 0));
+    __syncwarp();
+    return out;
+}
+
+template <int D, int SCHEME>
+__device__ __forceinline__ JobSetup setup_any(const SampleArgs& a, SlotT<D>& S, const TaskDesc t, int batch)
+{
+    if constexpr (D == 1) return setup_job1<SCHEME>(a, S, t, batch);
+    else return setup_job<D, SCHEME>(a, S, t, batch);
+}
+
+// d = 1 slot: the range holding concatenated index t of sequence (cc, k)
+__device__ __forceinline__ uint32_t locate(const Slot1& S, int npar, int cs, int cc, int k, uint32_t t, uint32_t& B)
+{
+    (void)npar;
+    (void)cs;
+    int r = 0;
+    while (r < 2 && S.rc[cc][k][r + 1] <= t) ++r;
+    B = S.rb[cc][k][r];
+    return S.rs[cc][k][r] + (t - S.rc[cc][k][r]);
+}
+
+__device__ __forceinline__ void locate_event(const Slot1& S, int clog2, int npar, int cs, int cc, int k, uint32_t nA,
+                                             uint32_t u, uint32_t& B, uint32_t& b0, uint32_t& nB, uint32_t& ch,
+                                             int& cl2)
+{
+    (void)npar;
+    (void)cs;
+    int r = 0;
+    while (r < 2 && S.rc[cc][k][r + 1] <= u) ++r;
+    B = S.rb[cc][k][r];
+    b0 = S.rs[cc][k][r];
+    nB = S.rn[cc][k][r];
+    ch = u - S.rc[cc][k][r];
+    const unsigned long long N = (unsigned long long)nA * (nB ? nB : 1u);
+    cl2 = chunk_log2(N, clog2, 15);
+}
+
 // concatenated index t (< M) of sequence (cc, k) -> sorted position in layer j and the cell
 template <int D>
 __device__ __forceinline__ uint32_t locate(const Slot<D>& S, int npar, int cs, int cc, int k, uint32_t t,
@@ -768,7 +957,7 @@ struct TileSource {
     }
 
     // set up the next job into S; false when the grid's tiles are exhausted
-    __device__ __noinline__ bool next(const SampleArgs& a, Slot<D>& S, unsigned long long& lo,
+    __device__ __noinline__ bool next(const SampleArgs& a, SlotT<D>& S, unsigned long long& lo,
                                          unsigned long long& hi, Counters& C)
     {
         const Plan* pl = a.pl;
@@ -796,7 +985,7 @@ struct TileSource {
                 t = make_task<D>(oi, task, ocode >> (D * ((int)pl->I[oi] - lg)));
                 batch = 0;
             }
-            const JobSetup js = setup_job<D, SCHEME>(a, S, t, batch);
+            const JobSetup js = setup_any<D, SCHEME>(a, S, t, batch);
             if (STATS && lane_id() == 0) C.ev2 += js.nseq2;
             const unsigned long long U = js.U, work = js.work;
             pend = (batch + 1) * Geo<D>::CB < js.nchild;
@@ -821,7 +1010,7 @@ struct TileSource {
 template <int D, int SCHEME, bool STATS>
 struct ItemSource {
     unsigned k, nit, stride;
-    __device__ __noinline__ bool next(const SampleArgs& a, Slot<D>& S, unsigned long long& lo,
+    __device__ __noinline__ bool next(const SampleArgs& a, SlotT<D>& S, unsigned long long& lo,
                                          unsigned long long& hi, Counters& C)
     {
         for (;;) {
@@ -829,7 +1018,7 @@ struct ItemSource {
             const BigItem it = a.items[k];
             k += stride;
             const TaskDesc t = make_task<D>(it.i, it.task, it.Cpar);
-            const JobSetup js = setup_job<D, SCHEME>(a, S, t, it.batch);  // sequences were counted by the job that queued it
+            const JobSetup js = setup_any<D, SCHEME>(a, S, t, it.batch);  // sequences were counted by the job that queued it
             (void)C;
 #ifdef GIRG_DEBUG
             if (js.U < it.hi && lane_id() == 0)
@@ -895,7 +1084,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         if (!T0 && (chain || pk == 0)) {
             uint4 ctr;
             if (chain) {
-                const Slot<D>& S = W.slot[ls];
+                const SlotT<D>& S = W.slot[ls];
                 const uint32_t A = S.seq[cc][kind].A;
                 ctr = SCHEME == SCHEME_MERGED ? make_uint4(A, ch, S.job.tag | ((uint32_t)(kind - 1) << 17) | (1u << 18), r)
                                               : make_uint4(A, Bev, S.job.tag | (ch << 17), r);
@@ -909,7 +1098,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         uint32_t npa = 0, npb = 0;
         double nra = 0.0, npbar = 1.0;
         if (chain) {
-            const Slot<D>& S = W.slot[ls];
+            const SlotT<D>& S = W.slot[ls];
             const Seq& Q = S.seq[cc][kind];
             ++r;
             if (STATS) ++C.draws;
@@ -944,7 +1133,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                     const uint32_t si = divmod(g, Q.M, ti);
                     uint32_t B;
                     npa = Q.a0 + si;
-                    npb = locate<D>(S, S.job.npar, S.job.cs, cc, kind, ti, B);
+                    npb = locate(S, S.job.npar, S.job.cs, cc, kind, ti, B);
                 } else {
                     uint32_t ti;
                     const uint32_t si = divmod(g, enB, ti);
@@ -1013,7 +1202,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         if (!chain && dnext < dhi) {
             const unsigned long long u = dnext + __popc(idle & ((1u << lane) - 1u));
             if (u < dhi) {
-                const Slot<D>& S = W.slot[ds];
+                const SlotT<D>& S = W.slot[ds];
                 int q = dq;  // sequence holding unit u
                 while (q < 3 * Geo<D>::CB - 1 && S.uoff[q + 1] <= u) ++q;
                 const int qc = q / 3, qk = q - 3 * qc;
@@ -1024,7 +1213,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                     const uint32_t si = divmod(x, Q.M, ti);
                     uint32_t B;
                     npa = Q.a0 + si;
-                    npb = locate<D>(S, S.job.npar, S.job.cs, qc, 0, ti, B);
+                    npb = locate(S, S.job.npar, S.job.cs, qc, 0, ti, B);
                     if (!(S.job.same_layer && B == Q.A && npb <= npa)) nk = 0;  // same cell: only s < t (R16)
                 } else {
                     chain = true;
@@ -1039,7 +1228,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                         end = (long long)min((unsigned long long)Q.nA * Q.M, st + (1ull << Q.cl2));
                     } else {
                         int c2;
-                        locate_event<D>(S, S.job.clog2[qk - 1], S.job.npar, S.job.cs, qc, qk, Q.nA, (uint32_t)x, Bev,
+                        locate_event(S, S.job.clog2[qk - 1], S.job.npar, S.job.cs, qc, qk, Q.nA, (uint32_t)x, Bev,
                                         eb0, enB, ch, c2);
                         const unsigned long long N = (unsigned long long)Q.nA * enB;
                         const unsigned long long st = (unsigned long long)ch << c2;
