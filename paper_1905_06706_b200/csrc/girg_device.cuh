@@ -155,20 +155,18 @@ __device__ __forceinline__ bool log2_split(double x, int& e, float& f)
     return ex != 0 && ex != 0x7ff && (b >> 63) == 0;
 }
 
-// r < min(1, ((wu*wv)*s / D)^invT) ?  1 / 0, or -1 when the float estimate cannot decide.
-// log2 ratio = sum of four log2_split terms (error <= 4 * 1.3e-6 + float rounding 7e-7 < 6e-6);
-// log2 r error <= 1.3e-6; margins 1e-5 (ratio vs 1) and 1e-5 * invT + 2e-6.
-__device__ __forceinline__ int fast_lt_prob(double r, double wu, double wv, double s, double Dp, double invT)
+// r < min(1, (q / D)^invT) with q = (wu*wv)*s (canonical, double) ?  1 / 0, or -1 when the float
+// estimate cannot decide.  log2 ratio = log2 q - log2 D (error <= 2 * 1.3e-6 + float rounding
+// 2.4e-7 < 3e-6); log2 r error <= 1.3e-6; margins 1e-5 (ratio vs 1) and 1e-5 * invT + 2e-6.
+__device__ __forceinline__ int fast_lt_prob(double r, double q, double Dp, double invT)
 {
-    int e1, e2, e3, e4, e5;
-    float f1, f2, f3, f4, f5;
-    bool ok = log2_split(wu, e1, f1);
-    ok &= log2_split(wv, e2, f2);
-    ok &= log2_split(s, e3, f3);
+    int e1, e4, e5;
+    float f1, f4, f5;
+    bool ok = log2_split(q, e1, f1);
     ok &= log2_split(Dp, e4, f4);
     ok &= log2_split(r, e5, f5);
     if (!ok) return -1;
-    const double lr = (double)(e1 + e2 + e3 - e4) + (double)((f1 + f2) + (f3 - f4));
+    const double lr = (double)(e1 - e4) + (double)(f1 - f4);
     if (lr > 1e-5) return 1;   // ratio > 1: p = 1 > r
     if (lr > -1e-5) return -1;
     const double diff = invT * lr - ((double)e5 + (double)f5);  // log2 p - log2 r

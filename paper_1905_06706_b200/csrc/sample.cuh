@@ -1152,7 +1152,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 // type-I: edge iff p >= 1 or r < p; type-II: edge iff r_acc * pbar < p (R14).
                 // Both are "x < p" with x < 1.
                 const double x = pk == 0 ? u53(o.x, o.y) : __dmul_rn(pra, ppbar);
-                const int fe = fast_lt_prob(x, wu, wv, s_, Dp, invT);
+                const int fe = fast_lt_prob(x, __dmul_rn(__dmul_rn(wu, wv), s_), Dp, invT);
                 edge = fe == 1;
                 if (STATS || fe < 0) {
                     const double p = exact_prob(wu, wv, s_, Dp, invT);
