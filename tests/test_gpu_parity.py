@@ -170,14 +170,30 @@ def test_degenerate_inputs():
     assert len(g) == 64 * 63 // 2
 
 
-def test_extreme_kappa():
-    n, d = 800, 2
+@SCHEMES
+@pytest.mark.parametrize("d", [1, 2, 3])
+def test_extreme_kappa(d, scheme):
+    """kappa so large that every level is coarse (CL <= 2: the whole-level regions of the job
+    setup, lg <= 1) or so small that only the finest cells matter."""
+    n = 800
     w, x = synth_inputs(n, d, 2.5, 4)
-    g, _, _ = assert_parity(w, x, d, 0.5, 1e6, 2)  # every pair saturated: complete graph
+    g, _, _ = assert_parity(w, x, d, 0.5, 1e6, 2, scheme=scheme)  # every pair saturated: complete graph
     assert len(g) == n * (n - 1) // 2
-    g, _, _ = assert_parity(w, x, d, 0.0, 1e-12, 2)
+    g, _, _ = assert_parity(w, x, d, 0.0, 1e-12, 2, scheme=scheme)
     assert len(g) == 0
-    assert_parity(w, x, d, 0.9, 1e-9, 2)
+    assert_parity(w, x, d, 0.9, 1e-9, 2, scheme=scheme)
+    for kappa in (3e-2, 0.3, 3.0, 30.0):  # CL of the heavy layers through 0, 1, 2
+        assert_parity(w, x, d, 0.6, kappa, 5, scheme=scheme)
+
+
+@pytest.mark.parametrize("d,T", [(1, 0.0), (1, 0.5), (2, 0.7), (3, 0.9)])
+def test_parity_over_edge_seeds(d, T):
+    """Several edge seeds on one graph (the draws differ per seed, the events do not)."""
+    n = 20_000
+    w, x = synth_inputs(n, d, 2.4, 90 + d)
+    kappa = O.scale_weights(w, 12.0, d, T, 2.4)
+    for seed in (1, 2, 3, 2**33 + 5):
+        assert_parity(w, x, d, T, kappa, seed)
 
 
 def test_capacity_and_determinism():
