@@ -58,6 +58,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef GIRG_NSLOT1
 #define GIRG_NSLOT1 3
 #endif
+#ifndef GIRG_MINB1
+#define GIRG_MINB1 2   // d = 1 resident blocks per SM (register cap)
+#endif
 #ifndef GIRG_NSLOT3
 #define GIRG_NSLOT3 2  // d = 3 job slots (development knob)
 #endif
@@ -72,7 +75,7 @@ struct Geo {
     static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // lg = 1: all 2^d level-1 cells
     static constexpr int CB = D <= 3 ? NCH : (D == 4 ? 4 : 2);        // children per job (batch)
     static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? 4 : 2);         // warps per block
-    static constexpr int MINB = D == 1 ? 2 : (D == 2 ? 3 : (D == 3 ? GIRG_MINB3 : 1));  // resident blocks per SM
+    static constexpr int MINB = D == 1 ? GIRG_MINB1 : (D == 2 ? 3 : (D == 3 ? GIRG_MINB3 : 1));  // resident blocks per SM
     static constexpr int NSLOT = D == 1 ? GIRG_NSLOT1 : (D == 2 ? 3 : (D == 3 ? GIRG_NSLOT3 : 2));  // job slots per warp
     static constexpr int RECW = D == 1 ? 2 : (D <= 3 ? 4 : 6);       // doubles per point record
 };
@@ -148,6 +151,7 @@ struct JobInfo {
     double pbar[2], Lbar[2];  // type-II bounds of kinds 1, 2 (R9)
     double il2[2];            // 1 / log2(1 - pbar) (fast jump path)
     int clog2[2];             // EVENT chunk length (R10)
+    int clog2m[2];            // MERGED chunk length (R22)
     uint32_t tag;             // l | i<<5 | j<<11
     int npar, cs, same_layer;
 };
@@ -351,6 +355,11 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
     const Plan* pl = a.pl;
     const unsigned lane = lane_id();
     const int nsub = 1 << t.cs;
+    // the type-II bounds of the job (lanes 0, 1: classes 2, 3), loaded before the region so that
+    // their latency overlaps the region loads
+    te = t.t2 ? a.tab + (pl->tab_off[t.i * MAXL + t.j] + 2u * (uint32_t)(t.l - 2)) : nullptr;
+    TabEntry tev = {0.0, 0.0, 0, 0, 0.0, 0.0};
+    if (te && lane < 2) tev = te[lane];
     // ---- region parents in Morton order ----
     if (t.lg >= 2) {
         uint32_t pc[D];
@@ -431,20 +440,20 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
     }
     const int nc = min(CB, out.nchild - batch * CB);
     if (nc <= 0) return 0;
-    te = t.t2 ? a.tab + (pl->tab_off[t.i * MAXL + t.j] + 2u * (uint32_t)(t.l - 2)) : nullptr;
     if (lane == 0) {
         JobInfo& J = S.job;
         J.tag = (uint32_t)t.l | ((uint32_t)t.i << 5) | ((uint32_t)t.j << 11);
         J.npar = t.npar;
         J.cs = t.cs;
         J.same_layer = t.i == t.j;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            J.pbar[k] = te ? te[k].pbar : 0.0;
-            J.Lbar[k] = te ? te[k].Lbar : 0.0;
-            J.il2[k] = te ? te[k].il2 : 0.0;
-            J.clog2[k] = te ? te[k].clog2 : 0;
-        }
+    }
+    if (lane < 2) {
+        JobInfo& J = S.job;
+        J.pbar[lane] = tev.pbar;
+        J.Lbar[lane] = tev.Lbar;
+        J.il2[lane] = tev.il2;
+        J.clog2[lane] = tev.clog2;
+        J.clog2m[lane] = tev.clog2m;
     }
     __syncwarp();
     return nc;
@@ -504,9 +513,9 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
                     uint32_t add = nB;
                     if (SCHEME == SCHEME_EVENT && kind > 0) {
                         add = 0;
-                        if (nB && te[kind - 1].pbar > 0.0) {
+                        if (nB && S.job.pbar[kind - 1] > 0.0) {
                             const unsigned long long N = (unsigned long long)nA * nB;
-                            add = (uint32_t)(((N - 1) >> chunk_log2(N, te[kind - 1].clog2, 15)) + 1);
+                            add = (uint32_t)(((N - 1) >> chunk_log2(N, S.job.clog2[kind - 1], 15)) + 1);
                         }
                     }
 #pragma unroll
@@ -572,9 +581,9 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
             uint32_t add = nB;
             if (SCHEME == SCHEME_EVENT && kind > 0) {  // chunks of the event (A, B)
                 add = 0;
-                if (nB && te[kind - 1].pbar > 0.0) {
+                if (nB && S.job.pbar[kind - 1] > 0.0) {
                     const unsigned long long N = (unsigned long long)nA * nB;
-                    add = (uint32_t)(((N - 1) >> chunk_log2(N, te[kind - 1].clog2, 15)) + 1);
+                    add = (uint32_t)(((N - 1) >> chunk_log2(N, S.job.clog2[kind - 1], 15)) + 1);
                 }
             }
 #pragma unroll
@@ -619,9 +628,9 @@ classified:
                 units[h] = (unsigned long long)Q.nA * acc;
             } else if (SCHEME == SCHEME_EVENT) {
                 units[h] = acc;
-            } else if (acc && te[k - 1].pbar > 0.0) {
+            } else if (acc && S.job.pbar[k - 1] > 0.0) {
                 const unsigned long long N = (unsigned long long)Q.nA * acc;
-                Q.cl2 = chunk_log2(N, te[k - 1].clog2m, 32);
+                Q.cl2 = chunk_log2(N, S.job.clog2m[k - 1], 32);
                 units[h] = ((N - 1) >> Q.cl2) + 1;
             }
         }
@@ -712,7 +721,7 @@ __device__ __noinline__ JobSetup setup_job1(const SampleArgs& a, Slot1& S, const
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             uint32_t acc = 0;
-            const TabEntry* tk = (k > 0 && t.t2) ? &te[k - 1] : nullptr;
+            const int kb = k > 0 ? k - 1 : 0;  // this kind's bound (JobInfo; zero when !t2)
             for (int r = 0; r < nk[k]; ++r) {
                 S.rs[cc][k][r] = cst[k][r];
                 S.rn[cc][k][r] = cn[k][r];
@@ -720,9 +729,9 @@ __device__ __noinline__ JobSetup setup_job1(const SampleArgs& a, Slot1& S, const
                 S.rc[cc][k][r] = acc;
                 if (k == 0 || SCHEME == SCHEME_MERGED) {
                     acc += cn[k][r];
-                } else if (cn[k][r] && tk->pbar > 0.0) {  // EVENT: chunks of the event (A, B)
+                } else if (cn[k][r] && S.job.pbar[kb] > 0.0) {  // EVENT: chunks of the event (A, B)
                     const unsigned long long N = (unsigned long long)nA * cn[k][r];
-                    acc += (uint32_t)(((N - 1) >> chunk_log2(N, tk->clog2, 15)) + 1);
+                    acc += (uint32_t)(((N - 1) >> chunk_log2(N, S.job.clog2[kb], 15)) + 1);
                 }
             }
             S.rc[cc][k][nk[k]] = acc;
@@ -738,9 +747,9 @@ __device__ __noinline__ JobSetup setup_job1(const SampleArgs& a, Slot1& S, const
                 units[k] = acc;
             } else {
                 Q.cl2 = 0;
-                if (acc && tk->pbar > 0.0) {
+                if (acc && S.job.pbar[kb] > 0.0) {
                     const unsigned long long N = (unsigned long long)nA * acc;
-                    Q.cl2 = chunk_log2(N, tk->clog2m, 32);
+                    Q.cl2 = chunk_log2(N, S.job.clog2m[kb], 32);
                     units[k] = ((N - 1) >> Q.cl2) + 1;
                 }
             }
@@ -917,6 +926,9 @@ struct TileSource {
     uint32_t total = 0, tk = 0;  // jobs of the tile (warp-uniform), next one
     int i = 0, lf = 255;         // this lane's point
     uint32_t code = 0, cnt = 0, start = 0;
+    uint32_t toffv = 0;          // its task list offset
+    int Ii = 0;                  // I(layer) of its point
+    uint16_t task32 = 0;         // task entry tk = lane of the tile (prefetched; tk >= 32 loads on demand)
     // pending task with further batches (d >= 4)
     bool pend = false;
     TaskDesc pt;
@@ -951,8 +963,18 @@ struct TileSource {
             }
         }
         cnt = lf == 255 ? 0u : pl->tcnt[i * 33 + lf];
+        toffv = lf == 255 ? 0u : pl->toff[i * 33 + lf];
+        Ii = pl->I[i];
         start = warp_excl_scan(cnt, total);
         tk = 0;
+        // prefetch the tile's first 32 task entries, one per lane (their loads overlap the jobs)
+        int owner = 0;
+        for (int src = 0; src < 32; ++src) {
+            const uint32_t sc = __shfl_sync(FULL, cnt, src), ss = __shfl_sync(FULL, start, src);
+            if (sc > 0 && ss <= lane) owner = src;
+        }
+        const uint32_t otoff = __shfl_sync(FULL, toffv, owner), ostart = __shfl_sync(FULL, start, owner);
+        task32 = lane < total ? __ldg(&a.tasks[otoff + (lane - ostart)]) : (uint16_t)0;
         return true;
     }
 
@@ -975,14 +997,19 @@ struct TileSource {
                 const unsigned own = __ballot_sync(FULL, cnt > 0 && start <= tk);
                 const int ol = 31 - __clz(own);
                 const int oi = __shfl_sync(FULL, i, ol);
-                const int olf = __shfl_sync(FULL, lf, ol);
                 const uint32_t ocode = __shfl_sync(FULL, code, ol);
-                const uint32_t ostart = __shfl_sync(FULL, start, ol);
-                GCHK(pl->toff[oi * 33 + olf] + (tk - ostart) < a.ntasks);
-                task = __ldg(&a.tasks[pl->toff[oi * 33 + olf] + (tk - ostart)]);
+                const int oI = __shfl_sync(FULL, Ii, ol);
+                const uint16_t tp = (uint16_t)__shfl_sync(FULL, (uint32_t)task32, tk & 31u);
+                if (tk < 32) {
+                    task = tp;
+                } else {
+                    const uint32_t ostart = __shfl_sync(FULL, start, ol), otoff = __shfl_sync(FULL, toffv, ol);
+                    GCHK(otoff + (tk - ostart) < a.ntasks);
+                    task = __ldg(&a.tasks[otoff + (tk - ostart)]);
+                }
                 ++tk;
                 const int lg = max(0, ((task >> 6) & 63) - Geo<D>::G);
-                t = make_task<D>(oi, task, ocode >> (D * ((int)pl->I[oi] - lg)));
+                t = make_task<D>(oi, task, ocode >> (D * (oI - lg)));
                 batch = 0;
             }
             const JobSetup js = setup_any<D, SCHEME>(a, S, t, batch);
