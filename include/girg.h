@@ -147,8 +147,10 @@ int girg_edges_ex(const double *w_dev, const double *x_dev, uint64_t n, int d, d
 
 /*
  * girg_edges_host -- end-to-end variant with HOST buffers: copies w_host[n] and x_host[d*n]
- * to the device, runs girg_edges and copies the edges back into edges_host[cap][2].
- * Pinned (page-locked) host memory gives full copy bandwidth.  Same semantics and errors.
+ * to the device and runs girg_edges.  If edges_host[cap][2] is page-locked (cudaHostAlloc /
+ * cudaHostRegister / torch pin_memory) the sampling kernels write the edges directly into it
+ * over the bus while they run; otherwise they are copied back after the run.  Same semantics
+ * and errors as girg_edges.
  */
 int girg_edges_host(const double *w_host, const double *x_host, uint64_t n, int d, double T,
                     double kappa, uint64_t seed, uint32_t *edges_host, uint64_t cap,

@@ -1193,12 +1193,23 @@ extern "C" int girg_edges_host(const double* w_host, const double* x_host, uint6
         Scratch S(st);
         double* w = S.alloc<double>(n);
         double* x = S.alloc<double>((size_t)d * n);
-        uint32_t* e = S.alloc<uint32_t>(2 * std::max<uint64_t>(cap, 1));
         GCHECK(cudaMemcpyAsync(w, w_host, n * sizeof(double), cudaMemcpyHostToDevice, st));
         GCHECK(cudaMemcpyAsync(x, x_host, (size_t)d * n * sizeof(double), cudaMemcpyHostToDevice, st));
+        // page-locked output: the sampling kernels write their staged edge blocks straight into
+        // host memory over the bus while they run (no device edge buffer, no trailing D2H copy)
+        uint32_t* mapped = nullptr;
+        if (cap) {
+            cudaPointerAttributes pa;
+            if (cudaPointerGetAttributes(&pa, edges_host) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+                pa.devicePointer)
+                mapped = (uint32_t*)pa.devicePointer;
+            cudaGetLastError();  // pageable memory: not an error, use the copy path
+        }
+        uint32_t* e = mapped ? mapped : S.alloc<uint32_t>(2 * std::max<uint64_t>(cap, 1));
         int rc = edges_impl(w, x, n, d, T, kappa, seed, 0, 0, 1, SCHEME_MERGED, e, cap, m_out, nullptr, st);
         if (rc != GIRG_OK) return rc;
-        if (*m_out) GCHECK(cudaMemcpyAsync(edges_host, e, *m_out * 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        if (*m_out && !mapped)
+            GCHECK(cudaMemcpyAsync(edges_host, e, *m_out * 2 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
         GCHECK(cudaStreamSynchronize(st));
         return GIRG_OK;
     } catch (const CudaFail& f) {

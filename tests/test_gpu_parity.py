@@ -252,7 +252,11 @@ def test_host_buffer_call_matches_device_call():
     ref = gpu_keys(girg.edges(dev(w), dev(x), T, kappa, 5))
     wh = torch.from_numpy(w).pin_memory()
     xh = torch.from_numpy(x).pin_memory()
-    out = torch.empty((len(ref) + 10, 2), dtype=torch.int32).pin_memory()
+    out = torch.empty((len(ref) + 10, 2), dtype=torch.int32).pin_memory()  # kernels write into it directly
     m = girg.edges_host(wh, xh, d, T, kappa, 5, out)
     assert m == len(ref)
     assert np.array_equal(girg.edge_keys(out[:m]).numpy().astype(np.uint64), ref)
+    pageable = torch.empty((len(ref) + 10, 2), dtype=torch.int32)  # copy-back path
+    m = girg.edges_host(torch.from_numpy(w), torch.from_numpy(x), d, T, kappa, 5, pageable)
+    assert m == len(ref)
+    assert np.array_equal(girg.edge_keys(pageable[:m]).numpy().astype(np.uint64), ref)
