@@ -137,7 +137,7 @@ struct SampleArgs {
     unsigned int ntab, ntasks;
     unsigned long long big_work, item_work;  // job split thresholds (BIG_WORK / ITEM_WORK by default)
     unsigned long long* wprof;               // optional per-warp profile: cycles, jobs, iterations, lane steps
-    unsigned dev_flags;                      // development: 1 = set up jobs but skip their units
+    unsigned dev_flags;                      // development (-DGIRG_PROFILE builds): 1 = set up jobs, skip units
 };
 
 struct TaskDesc {
@@ -1082,8 +1082,10 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
     const unsigned lane = lane_id();
     const bool T0 = pl->T == 0.0;
     const double s_ = pl->s, invT = pl->invT;
+#ifdef GIRG_PROFILE
     const long long t_start = clock64();
     unsigned long long n_jobs = 0, n_iter = 0, n_steps = 0;
+#endif
     unsigned fill = 0;
     int ds = 0, dq = 0;  // dispatch slot, its first sequence with units left
     unsigned long long dnext = 0, dhi = 0;
@@ -1102,10 +1104,12 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
 #pragma unroll
     for (int k = 0; k < D; ++k) xu[k] = xv[k] = 0.0;
     for (;;) {
+#ifdef GIRG_PROFILE
         if (a.wprof) {
             ++n_iter;
             n_steps += __popc(__ballot_sync(FULL, chain || pk >= 0));
         }
+#endif
         // ---- (1) one Philox block per lane ----
         uint4 o = make_uint4(0u, 0u, 0u, 0u);
         if (!T0 && (chain || pk == 0)) {
@@ -1213,9 +1217,11 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
             if (ns < Geo<D>::NSLOT) {
                 unsigned long long lo, hi;
                 if (src.next(a, W.slot[ns], lo, hi, C)) {
+#ifdef GIRG_PROFILE
                     ++n_jobs;
-                    ds = ns;
                     if (a.dev_flags & 1) lo = hi;
+#endif
+                    ds = ns;
                     dnext = lo;
                     dhi = hi;
                     dq = 0;
@@ -1288,6 +1294,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         if (!more && dnext >= dhi && !__any_sync(FULL, chain || pk >= 0)) break;
     }
     warp_flush(a, W.ebuf, fill);
+#ifdef GIRG_PROFILE
     if (a.wprof && lane == 0) {
         const unsigned w = blockIdx.x * Geo<D>::WPB + (threadIdx.x >> 5);
         unsigned long long* op = a.wprof + 4ull * w;
@@ -1296,6 +1303,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         op[2] += n_iter;
         op[3] += n_steps;
     }
+#endif
 }
 
 template <int D, int SCHEME, bool STATS>

@@ -1,4 +1,5 @@
-"""Summarise a GIRG_WARP_PROFILE dump (per-warp cycles, jobs, engine iterations, lane steps)."""
+"""Summarise a GIRG_WARP_PROFILE dump (per-warp cycles, jobs, engine iterations, lane steps).
+The counters exist only in libraries built with -DGIRG_PROFILE (development builds)."""
 import sys
 
 import numpy as np
