@@ -960,6 +960,27 @@ struct Estimator {
     double T, W, wmax, tau;
     TailSums tail;                // fixed-order sum of the block partials
     std::vector<double> cand;     // weights > tau, decreasing
+    std::vector<double> zeta;     // (cand / wmax)^(1/T), computed once per tau (set_cand)
+    std::vector<double> sc1, sc2, sz1, sz2;  // suffix sums of cand, cand^2, zeta, zeta^2 (from k on)
+    mutable std::vector<double> S1s, SPs;  // scratch of f (no allocation per evaluation)
+
+    void set_cand()
+    {
+        const double invT = T > 0.0 ? 1.0 / T : 0.0;
+        const size_t nc = cand.size();
+        zeta.resize(nc);
+        for (size_t k = 0; k < nc; ++k) zeta[k] = T > 0.0 ? std::pow(cand[k] / wmax, invT) : 0.0;
+        sc1.assign(nc + 1, 0.0);
+        sc2.assign(nc + 1, 0.0);
+        sz1.assign(nc + 1, 0.0);
+        sz2.assign(nc + 1, 0.0);
+        for (size_t k = nc; k-- > 0;) {  // ascending weights: small terms first
+            sc1[k] = sc1[k + 1] + cand[k];
+            sc2[k] = sc2[k + 1] + cand[k] * cand[k];
+            sz1[k] = sz1[k + 1] + zeta[k];
+            sz2[k] = sz2[k + 1] + zeta[k] * zeta[k];
+        }
+    }
 
     // f(kappa); returns false if tau is not small enough for this kappa (R must lie in cand)
     bool f(double kappa, double& out) const
@@ -972,15 +993,13 @@ struct Estimator {
         // R = prefix of cand with (a w) wmax > 1
         size_t nr = 0;
         while (nr < nc && (a * cand[nr]) * wmax > 1.0) ++nr;
-        std::vector<double> zeta(nc), S1s(nr + 1), SPs(nr + 1);
-        for (size_t k = 0; k < nc; ++k) zeta[k] = T > 0.0 ? std::pow(cand[k] / wmax, invT) : 0.0;
-        double Wsmall = tail.s1, Zs = tail.z1, W2s = tail.s2, Z2s = tail.z2;
-        for (size_t k = nr; k < nc; ++k) {  // candidates outside R
-            Wsmall += cand[k];
-            W2s += cand[k] * cand[k];
-            Zs += zeta[k];
-            Z2s += zeta[k] * zeta[k];
+        if (S1s.size() < nr + 1) {
+            S1s.resize(nr + 1);
+            SPs.resize(nr + 1);
         }
+        // candidates outside R (suffix sums, O(1) per evaluation)
+        const double Wsmall = tail.s1 + sc1[nr], Zs = tail.z1 + sz1[nr], W2s = tail.s2 + sc2[nr],
+                     Z2s = tail.z2 + sz2[nr];
         S1s[nr] = 0.0;
         SPs[nr] = 0.0;
         for (size_t k = nr; k-- > 0;) {
@@ -1034,6 +1053,7 @@ static void estimator_tail(const double* w, uint64_t n, Estimator& E, cudaStream
             GCHECK(cudaStreamSynchronize(st));
         }
         std::sort(E.cand.begin(), E.cand.end(), [](double x, double y) { return x > y; });
+        E.set_cand();
         E.tail = TailSums{0, 0, 0, 0};
         for (const TailSums& t : hp) {
             E.tail.s1 += t.s1; E.tail.s2 += t.s2; E.tail.z1 += t.z1; E.tail.z2 += t.z2;

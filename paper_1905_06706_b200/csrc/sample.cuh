@@ -465,7 +465,6 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
     JobSetup out = {0ull, 0ull, 0, 0};
     constexpr int NCH = Geo<D>::NCH, CB = Geo<D>::CB;
     using MaskT = typename Slot<D>::MaskT;
-    const Plan* pl = a.pl;
     const unsigned lane = lane_id();
     const int nsub = 1 << t.cs;
     const TabEntry* te = nullptr;
@@ -476,6 +475,7 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
     const uint32_t side = 1u << t.l, msk = side - 1u;
     const uint32_t side2 = side >> 1, msk2 = side2 - 1u;  // level l-1 (parent check, G > 1)
     const bool pcheck = Geo<D>::G > 1 && t.l >= 3;
+    bool separable = false;  // classified by the separable path below
     if constexpr (Geo<D>::G == 1 && D <= 3) {
         if (t.l >= 1) {  // sub-cells = the 2^d children of each region parent: separable per dimension
             for (int idx = lane; idx < nc * t.npar; idx += 32) {
@@ -531,10 +531,10 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
                     S.pre[cc][kk][q] = cnt[kk];
                 }
             }
-            goto classified;
+            separable = true;
         }
     }
-    for (int idx = lane; idx < nc * t.npar; idx += 32) {
+    for (int idx = lane; !separable && idx < nc * t.npar; idx += 32) {
         const int cc = idx / t.npar, q = idx - cc * t.npar;
         const int e = S.child[cc];
         const uint32_t A = (t.Cpar << t.cs) + (uint32_t)e;
@@ -599,7 +599,6 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
             S.pre[cc][kk][q] = cnt[kk];
         }
     }
-classified:
     __syncwarp();
     // ---- phase 2: per (child, kind): prefix over parents and the sequence (<= 2 per lane) ----
     constexpr int NE = (3 * CB + 31) / 32;
@@ -982,7 +981,6 @@ struct TileSource {
     __device__ __noinline__ bool next(const SampleArgs& a, SlotT<D>& S, unsigned long long& lo,
                                          unsigned long long& hi, Counters& C)
     {
-        const Plan* pl = a.pl;
         for (;;) {
             TaskDesc t;
             uint16_t task;
