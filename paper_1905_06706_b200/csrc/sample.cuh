@@ -985,7 +985,8 @@ struct TileSource {
             TaskDesc t;
             uint16_t task;
             int batch;
-            if (pend) {
+            constexpr bool multi = Geo<D>::CB < Geo<D>::NCH;  // d >= 4: a task may need several batches
+            if (multi && pend) {
                 t = pt;
                 task = ptask;
                 batch = pbatch;
@@ -1013,8 +1014,8 @@ struct TileSource {
             const JobSetup js = setup_any<D, SCHEME>(a, S, t, batch);
             if (STATS && lane_id() == 0) C.ev2 += js.nseq2;
             const unsigned long long U = js.U, work = js.work;
-            pend = (batch + 1) * Geo<D>::CB < js.nchild;
-            if (pend) {
+            pend = multi && (batch + 1) * Geo<D>::CB < js.nchild;
+            if (multi && pend) {
                 pt = t;
                 ptask = task;
                 pbatch = batch + 1;
