@@ -58,6 +58,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef GIRG_NSLOT1
 #define GIRG_NSLOT1 3
 #endif
+#ifndef GIRG_WPB3
+#define GIRG_WPB3 4    // d = 3 warps per block
+#endif
 #ifndef GIRG_MINB1
 #define GIRG_MINB1 2   // d = 1 resident blocks per SM (register cap)
 #endif
@@ -74,7 +77,7 @@ struct Geo {
     static constexpr int NPAR = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : 243;  // 3^d
     static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // lg = 1: all 2^d level-1 cells
     static constexpr int CB = D <= 3 ? NCH : (D == 4 ? 4 : 2);        // children per job (batch)
-    static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? 4 : 2);         // warps per block
+    static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? GIRG_WPB3 : 2);  // warps per block
     static constexpr int MINB = D == 1 ? GIRG_MINB1 : (D == 2 ? 3 : (D == 3 ? GIRG_MINB3 : 1));  // resident blocks per SM
     static constexpr int NSLOT = D == 1 ? GIRG_NSLOT1 : (D == 2 ? 3 : (D == 3 ? GIRG_NSLOT3 : 2));  // job slots per warp
     static constexpr int RECW = D == 1 ? 2 : (D <= 3 ? 4 : 6);       // doubles per point record
