@@ -45,7 +45,10 @@
 #endif
 
 constexpr int SCHEME_EVENT = 0, SCHEME_MERGED = 1;
-constexpr int EB = 128;                          // staged edges per warp
+#ifndef GIRG_EB
+#define GIRG_EB 128
+#endif
+constexpr int EB = GIRG_EB;                      // staged edges per warp
 // weighted units (a chunk counts 8) above which a job is queued for k_big, and per queued item
 __host__ __device__ constexpr unsigned long long big_work(int d) { return d == 1 ? 512ull : (d == 2 ? 2048ull : 32768ull); }
 __host__ __device__ constexpr unsigned long long item_work(int d) { return d == 1 ? 256ull : (d == 2 ? 1024ull : 16384ull); }
