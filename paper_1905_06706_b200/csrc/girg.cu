@@ -6,11 +6,11 @@
 //   K1 k_keys       layer + Morton cell at the insertion level, histogram over the cell space
 //   K2 k_scan_*     exclusive scan of the cell histogram = the prefix arrays P_C of Lemma 1
 //   K3 k_scatter    slot of every vertex in its cell
-//   K4 k_gather     in-cell order by vertex id (R11) + gather of x, w, id into sorted SoA
-//   K5 k_sample     per (layer pair, level, A cell): type-I pair tests and type-II geometric
-//                   jumps (Algorithm 1 events), warp-aggregated edge output
+//   K4 k_order      in-cell order by vertex id (R11); k_place: sorted AoS point records
+//   K5 k_sample     jobs (layer pair, level, task cell): type-I pair tests and type-II geometric
+//                   jumps (Algorithm 1 events), warp-staged edge output; k_big runs
+//                   the unit ranges of queued big jobs (csrc/sample.cuh)
 // Citations "P:NNN" are lines of PAPER.md (arXiv:1905.06706); R* are DESIGN.md readings.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -26,8 +26,6 @@
 
 #include "../../include/girg.h"
 #include "girg_device.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace girg {
 
