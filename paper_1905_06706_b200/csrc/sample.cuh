@@ -818,11 +818,13 @@ template <int D>
 __device__ __forceinline__ uint32_t locate(const Slot<D>& S, int npar, int cs, int cc, int k, uint32_t t,
                                            uint32_t& B)
 {
-    int lo = 0, hi = npar - 1;  // last parent with pre <= t
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (S.pre[cc][k][mid] <= t) lo = mid;
-        else hi = mid - 1;
+    // last parent with pre <= t: fixed-step branchless search (pre[npar] = total > t stops it)
+    constexpr int TOP = Geo<D>::MAXPAR >= 128 ? 128 : (Geo<D>::MAXPAR >= 64 ? 64 : (Geo<D>::MAXPAR >= 32 ? 32 : (Geo<D>::MAXPAR >= 16 ? 16 : (Geo<D>::MAXPAR >= 8 ? 8 : (Geo<D>::MAXPAR >= 4 ? 4 : 2)))));
+    int lo = 0;
+#pragma unroll
+    for (int step = TOP; step; step >>= 1) {
+        const int m = lo + step;
+        if (S.pre[cc][k][min(m, npar)] <= t) lo = m;
     }
     uint32_t r = t - S.pre[cc][k][lo];
     uint32_t m = S.mask[cc][k][lo];
