@@ -74,6 +74,9 @@ def test_argument_validation_before_launch(girg):
     assert L.girg_scale_weights(1234, 10, 9.0, 1, 0.5, 2.5, C.byref(k), None) == girg.EINVAL  # avg_deg >= n-1
     assert L.girg_scale_weights(1234, 10, 1.0, 1, 0.5, 2.0, C.byref(k), None) == girg.EINVAL  # beta
     assert L.girg_edges_host(None, 1234, 10, 1, 0.5, 1.0, 1, 1234, 10, C.byref(m), None) == girg.EINVAL
+    for bad in (girg.Options(7, 0, 0, 1), girg.Options(-1, 0, 0, 1), girg.Options(girg.SCHEME_EVENT, 0, 1, 1)):
+        assert L.girg_edges_ex(1234, 1234, 10, 2, 0.5, 1.0, 1, C.byref(bad), 1234, 10, C.byref(m), None,
+                               None) == girg.EINVAL  # unknown scheme / empty block range
 
 
 def test_product_path_is_independent_of_the_oracle():
