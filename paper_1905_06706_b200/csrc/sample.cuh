@@ -306,6 +306,10 @@ __device__ __noinline__ uint32_t divmod64(unsigned long long x, uint32_t m, uint
 }
 __device__ __forceinline__ uint32_t divmod(unsigned long long x, uint32_t m, uint32_t& rem)
 {
+    if (x < m) {  // the common case at fine levels: A holds one point, so every index is in row 0
+        rem = (uint32_t)x;
+        return 0u;
+    }
     if (x <= 0xFFFFFFFFull) {
         const uint32_t q = (uint32_t)x / m;
         rem = (uint32_t)x - q * m;
