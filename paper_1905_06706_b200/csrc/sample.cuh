@@ -55,23 +55,30 @@ __host__ __device__ constexpr unsigned long long item_work(int d) { return d == 
 constexpr int ERR_ITEMS = 16;
 constexpr unsigned FULL = 0xffffffffu;
 
+// Tuning knobs (compile-time; the defaults are the B200 sweep optima recorded in
+// profiles/r01/SUMMARY.md; tools/sweep_*.sh rebuild variants with -D to re-tune):
+//   GIRG_G1      d = 1 task height: a job covers the 2^G1 level-l cells below one task cell
+//   GIRG_NSLOT1  d = 1 job slots per warp;  GIRG_MINB1  d = 1 resident blocks per SM
+//   GIRG_WPB3    d = 3 warps per block;     GIRG_NSLOT3 / GIRG_MINB3  d = 3 slots / blocks per SM
+//   GIRG_EB      staged edges per warp
+// GIRG_PROFILE adds per-warp cycle / job / iteration counters (GIRG_WARP_PROFILE dumps them).
 #ifndef GIRG_G1
-#define GIRG_G1 4  // d = 1 task height (development knob)
+#define GIRG_G1 4
 #endif
 #ifndef GIRG_NSLOT1
 #define GIRG_NSLOT1 3
 #endif
 #ifndef GIRG_WPB3
-#define GIRG_WPB3 4    // d = 3 warps per block
+#define GIRG_WPB3 4
 #endif
 #ifndef GIRG_MINB1
-#define GIRG_MINB1 2   // d = 1 resident blocks per SM (register cap)
+#define GIRG_MINB1 2
 #endif
 #ifndef GIRG_NSLOT3
-#define GIRG_NSLOT3 2  // d = 3 job slots (development knob)
+#define GIRG_NSLOT3 2
 #endif
 #ifndef GIRG_MINB3
-#define GIRG_MINB3 4   // d = 3 resident blocks per SM (register cap)
+#define GIRG_MINB3 4
 #endif
 template <int D>
 struct Geo {
