@@ -495,12 +495,15 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
     bool separable = false;  // classified by the separable path below
     if constexpr (Geo<D>::G == 1 && D <= 3) {
         if (t.l >= 1) {  // sub-cells = the 2^d children of each region parent: separable per dimension
+            uint32_t cpc[D];  // coordinates of the task cell (level l-1)
+            morton_decode<D>(t.Cpar, cpc);
             for (int idx = lane; idx < nc * t.npar; idx += 32) {
                 const int cc = idx / t.npar, q = idx - cc * t.npar;
                 const int e = S.child[cc];
-                const uint32_t A = (t.Cpar << D) + (uint32_t)e, P = S.par[q];
+                const uint32_t P = S.par[q];
                 uint32_t ac[D], pc[D], g0[D], g1[D];
-                morton_decode<D>(A, ac);
+#pragma unroll
+                for (int k = 0; k < D; ++k) ac[k] = (cpc[k] << 1) | (((uint32_t)e >> (D - 1 - k)) & 1u);
                 morton_decode<D>(P, pc);
 #pragma unroll
                 for (int k = 0; k < D; ++k) {  // torus gaps of the two children per dimension
@@ -514,6 +517,35 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
 #pragma unroll
                 for (int k = 0; k <= NCH; ++k) rs[k] = S.rstart[q][k];
                 uint32_t cnt[3] = {0u, 0u, 0u}, m[3] = {0u, 0u, 0u};
+                if constexpr (SCHEME == SCHEME_MERGED) {
+                    // Sub-cell sets as bit masks: {s : max_k gap_k(s) <= tau} is the AND over the
+                    // dimensions of the sub-cells whose own gap in that dimension is <= tau.
+                    constexpr uint32_t FULLN = (1u << NCH) - 1u;
+                    uint32_t le1 = FULLN, le2 = FULLN;
+#pragma unroll
+                    for (int k = 0; k < D; ++k) {
+                        uint32_t p1 = 0u;
+#pragma unroll
+                        for (int sc = 0; sc < NCH; ++sc) p1 |= ((sc >> (D - 1 - k)) & 1) ? (1u << sc) : 0u;
+                        const uint32_t p0 = FULLN ^ p1;
+                        le1 &= (g0[k] <= 1u ? p0 : 0u) | (g1[k] <= 1u ? p1 : 0u);
+                        le2 &= (g0[k] <= 2u ? p0 : 0u) | (g1[k] <= 2u ? p1 : 0u);
+                    }
+                    uint32_t GE = FULLN, GT = FULLN;  // sub-cells B with (i < j or B >= / > A)
+                    if (!(t.i < t.j || pcmp > 0)) {
+                        GE = pcmp < 0 ? 0u : (FULLN << e) & FULLN;
+                        GT = pcmp < 0 ? 0u : (FULLN << (e + 1)) & FULLN;
+                    }
+                    m[0] = t.t1 ? (le1 & GE) : 0u;
+                    m[1] = t.t2 ? (le2 & ~le1 & GT) : 0u;
+                    m[2] = t.t2 ? (~le2 & GT & FULLN) : 0u;
+#pragma unroll
+                    for (int sc = 0; sc < NCH; ++sc) {
+                        const uint32_t nB = rs[sc + 1] - rs[sc];
+#pragma unroll
+                        for (int kk = 0; kk < 3; ++kk) cnt[kk] += ((m[kk] >> sc) & 1u) ? nB : 0u;
+                    }
+                } else {
 #pragma unroll
                 for (int sc = 0; sc < NCH; ++sc) {
                     uint32_t dm = 0;
@@ -541,6 +573,7 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
                             m[kk] |= 1u << sc;
                             cnt[kk] += add;
                         }
+                }
                 }
 #pragma unroll
                 for (int kk = 0; kk < 3; ++kk) {
