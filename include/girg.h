@@ -156,6 +156,30 @@ int girg_edges_host(const double *w_host, const double *x_host, uint64_t n, int 
                     double kappa, uint64_t seed, uint32_t *edges_host, uint64_t cap,
                     uint64_t *m_out, void *stream);
 
+/*
+ * girg_edges_batch -- many independent GIRGs in one call ("batched small
+ * graphs"; the paper's observation that many instances of a generator beat one parallel
+ * instance for small n).  Graph g is exactly girg_edges(w_dev[g], x_dev[g], n, d, T,
+ * kappa[g], seed[g], edges_dev[g], cap[g], &m_out[g], .) -- the same edge set, bit for bit.
+ *   B            number of graphs (>= 1); all share n, d and T
+ *   w_dev, x_dev host arrays of B device pointers: w[n] and x[d][n] (SoA) of each graph
+ *   kappa, seed  host arrays [B]
+ *   edges_dev    host array of B device pointers to caller-owned uint32 [cap[g]][2] buffers
+ *   cap          host array [B]
+ *   m_out        host array [B]: the true edge count of each graph (also when > cap[g])
+ *   status_out   host array [B] or NULL: the girg_status of each graph
+ *   nstreams     concurrency: graphs run as independent pipelines on this many internal
+ *                streams, one native host thread each (0 = default 8; clamped to [1, B])
+ *   stream       ordering: the batch starts after the work already queued on `stream` and the
+ *                call returns when every graph is done (it synchronises, as girg_edges does)
+ * Returns GIRG_OK if every graph succeeded, else the status of the lowest failing index
+ * (GIRG_ECAPACITY included); EINVAL for B < 1 or NULL arrays.
+ */
+int girg_edges_batch(int B, const double *const *w_dev, const double *const *x_dev, uint64_t n,
+                     int d, double T, const double *kappa, const uint64_t *seed,
+                     uint32_t *const *edges_dev, const uint64_t *cap, uint64_t *m_out,
+                     int *status_out, int nstreams, void *stream);
+
 /* Phase timings of the last successful girg_edges / girg_edges_shard / girg_edges_host call on
  * the calling host thread, measured with CUDA events recorded on the call's stream around each
  * phase (the events cost ~1 us; they are always recorded). */

@@ -64,16 +64,17 @@ _lib.girg_edges_shard.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, _i, _u64, _u
 _lib.girg_edges_ex.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, C.POINTER(Options), _vp, _u64,
                                C.POINTER(_u64), C.POINTER(Stats), _vp]
 _lib.girg_edges_host.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, _vp, _u64, C.POINTER(_u64), _vp]
+_lib.girg_edges_batch.argtypes = [_i, _vp, _vp, _u64, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp]
 _lib.girg_last_timings.argtypes = [C.POINTER(Timings)]
 _lib.girg_strerror.argtypes = [_i]
 _lib.girg_strerror.restype = C.c_char_p
 _lib.girg_last_cuda_error.restype = C.c_char_p
 for _f in ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
-           "girg_edges_ex", "girg_edges_host", "girg_version", "girg_last_timings"):
+           "girg_edges_ex", "girg_edges_host", "girg_edges_batch", "girg_version", "girg_last_timings"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTS = ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
-           "girg_edges_ex", "girg_edges_host", "girg_strerror", "girg_last_cuda_error", "girg_version", "girg_last_timings")
+           "girg_edges_ex", "girg_edges_host", "girg_edges_batch", "girg_strerror", "girg_last_cuda_error", "girg_version", "girg_last_timings")
 
 
 class GirgError(RuntimeError):
@@ -174,6 +175,40 @@ def edges_host(w_host, x_host, d: int, T: float, kappa: float, seed: int, out_ho
     _check(_lib.girg_edges_host(w_host.data_ptr(), x_host.data_ptr(), n, d, T, kappa, seed, out_host.data_ptr(),
                                 out_host.shape[0], C.byref(m), _stream(stream)))
     return int(m.value)
+
+
+def edges_batch(ws, xs, T: float, kappas, seeds, caps=None, nstreams: int = 8, stream=None):
+    """Many independent graphs in one call (include/girg.h girg_edges_batch): graph g equals
+    edges(ws[g], xs[g], T, kappas[g], seeds[g]).  Returns a list of int32 CUDA tensors [m_g, 2];
+    graphs whose capacity was too small are re-issued once, individually, with the exact size."""
+    B = len(ws)
+    if not (len(xs) == len(kappas) == len(seeds) == B) or B < 1:
+        raise ValueError("ws, xs, kappas, seeds must have the same length >= 1")
+    n = ws[0].numel()
+    d = xs[0].numel() // n
+    for w, x in zip(ws, xs):
+        _dev_f64(w, "w")
+        _dev_f64(x, "x")
+        if w.numel() != n or x.numel() != d * n:
+            raise ValueError("all graphs must share n and d")
+    if caps is None:
+        caps = [16 * n + 1024] * B
+    bufs = [torch.empty((int(c), 2), dtype=torch.int32, device=ws[0].device) for c in caps]
+    P = C.c_void_p * B
+    pw, px, pe = P(*[w.data_ptr() for w in ws]), P(*[x.data_ptr() for x in xs]), P(*[b.data_ptr() for b in bufs])
+    ka, se = (_d * B)(*[float(k) for k in kappas]), (_u64 * B)(*[int(s) for s in seeds])
+    ca, mo, so = (_u64 * B)(*[int(c) for c in caps]), (_u64 * B)(), (_i * B)()
+    rc = _lib.girg_edges_batch(B, pw, px, n, d, T, ka, se, pe, ca, mo, so, nstreams, _stream(stream))
+    out = []
+    for g in range(B):
+        if so[g] == ECAPACITY:
+            out.append(edges(ws[g], xs[g], T, kappas[g], seeds[g], cap=int(mo[g]), stream=stream))
+            continue
+        _check(so[g])
+        out.append(bufs[g][: mo[g]])
+    if rc not in (0, ECAPACITY):
+        _check(rc)
+    return out
 
 
 def last_timings() -> dict:

@@ -21,7 +21,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/girg.h"
@@ -372,16 +375,56 @@ thread_local std::string g_last_cuda;
 thread_local girg_timings g_timings;
 
 // CUDA events around the phases of one call (recorded on the call's stream)
-struct PhaseEvents {
+// Per-call host resources (timing events, a page-locked staging buffer) come from a process-wide
+// pool: a call borrows one set and returns it, so repeated and concurrent calls (girg_edges_batch)
+// do not create and destroy driver objects every time.
+struct HostRes {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    char* pinned = nullptr;  // page-locked staging (plan upload, status download)
+    size_t cap = 0;
+};
+
+static std::mutex g_res_mu;
+static std::vector<HostRes*> g_res_free;
+
+struct PhaseEvents {
+    HostRes* r = nullptr;
+    cudaEvent_t* ev = nullptr;
     PhaseEvents()
     {
-        for (auto& e : ev) cudaEventCreate(&e);
+        {
+            std::lock_guard<std::mutex> lk(g_res_mu);
+            if (!g_res_free.empty()) {
+                r = g_res_free.back();
+                g_res_free.pop_back();
+            }
+        }
+        if (!r) {
+            r = new HostRes;
+            for (auto& e : r->ev) cudaEventCreate(&e);
+        }
+        ev = r->ev;
     }
     ~PhaseEvents()
     {
-        for (auto& e : ev)
-            if (e) cudaEventDestroy(e);
+        std::lock_guard<std::mutex> lk(g_res_mu);
+        g_res_free.push_back(r);
+    }
+    // page-locked staging of at least `bytes` (valid until the next staging() of this call)
+    char* staging(size_t bytes)
+    {
+        if (r->cap < bytes) {
+            if (r->pinned) cudaFreeHost(r->pinned);
+            r->pinned = nullptr;
+            r->cap = 0;
+            const size_t want = std::max<size_t>(bytes, 1 << 16);
+            if (cudaHostAlloc((void**)&r->pinned, want, cudaHostAllocDefault) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+            r->cap = want;
+        }
+        return r->pinned;
     }
     void record(int k, cudaStream_t st) { cudaEventRecord(ev[k], st); }
     double ms(int a, int b) const
@@ -425,9 +468,24 @@ struct Scratch {
         cudaGetDevice(&dev);
         pool_keep(dev);
     }
+    char* arena = nullptr;  // one block carved by alloc() (reserve()); 256-B aligned pieces
+    size_t acap = 0, aoff = 0;
+    static size_t rounded(size_t bytes) { return (std::max<size_t>(bytes, 16) + 255) & ~(size_t)255; }
+    void reserve(size_t bytes)
+    {
+        arena = alloc<char>(bytes);
+        acap = bytes;
+        aoff = 0;
+    }
     template <class T>
     T* alloc(size_t count)
     {
+        const size_t r = rounded(count * sizeof(T));
+        if (arena && aoff + r <= acap) {
+            T* q = (T*)(arena + aoff);
+            aoff += r;
+            return q;
+        }
         void* p = nullptr;
         const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
         cudaError_t e = cudaMallocAsync(&p, bytes, st);
@@ -684,17 +742,31 @@ static void launch_sample_t(const SampleArgs& a, cudaStream_t st)
     const size_t smem = sizeof(WarpSmem<D>) * WPB;
     smem_optin(k_sample<D, SCHEME, STATS>, smem);
     smem_optin(k_big<D, SCHEME, STATS>, smem);
-    int dev = 0, nsm = 148, occ = 1, occ2 = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sample<D, SCHEME, STATS>, TPB, smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_big<D, SCHEME, STATS>, TPB, smem);
+    // SM count and occupancies queried once per instantiation (one GPU type per process)
+    static const int nsm = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    static const int occ = [] {
+        int v = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_sample<D, SCHEME, STATS>, TPB, sizeof(WarpSmem<D>) * WPB);
+        return v;
+    }();
+    static const int occ2 = [] {
+        int v = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_big<D, SCHEME, STATS>, TPB, sizeof(WarpSmem<D>) * WPB);
+        return v;
+    }();
     const unsigned wtiles = (a.ntiles + WPB - 1) / WPB;
     unsigned grid = std::max(1u, std::min<unsigned>(wtiles, (unsigned)(nsm * std::max(occ, 1))));
     if (const char* g = getenv("GIRG_SAMPLE_GRID")) grid = std::max(1u, std::min<unsigned>(wtiles, (unsigned)atoi(g)));
     static const bool sync_debug = getenv("GIRG_SYNC_DEBUG") != nullptr;
     static const char* wprof_path = getenv("GIRG_WARP_PROFILE");  // development: per-warp profile dump
-    const unsigned gbig = (unsigned)(nsm * std::max(occ2, 1));
+    // k_big: a full wave, but no wider than k_sample's grid (small graphs leave the rest of the
+    // GPU to concurrent calls, girg_edges_batch)
+    const unsigned gbig = std::min<unsigned>(grid, (unsigned)(nsm * std::max(occ2, 1)));
     const size_t nwarps = (size_t)std::max(grid, gbig) * WPB;
     SampleArgs b = a;
     if (wprof_path) {
@@ -771,10 +843,18 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         hp.p.bhi = bhi;
         const uint32_t n32 = (uint32_t)n;
         const uint64_t K = hp.K;
-        // scratch
-        Plan* d_plan = S.alloc<Plan>(1);
-        TabEntry* d_tab = S.alloc<TabEntry>(hp.tab.size());
-        uint16_t* d_tasks = S.alloc<uint16_t>(hp.tasks.size());
+        // scratch: one stream-ordered block for everything this call needs
+        const int recw = d == 1 ? 2 : (d <= 3 ? 4 : 6);
+        unsigned int items_cap = std::max<unsigned int>(1u << 18, n32 / 2);
+        const size_t up_plan = Scratch::rounded(sizeof(Plan)), up_tab = Scratch::rounded(hp.tab.size() * sizeof(TabEntry)),
+                     up_bytes = up_plan + up_tab + hp.tasks.size() * sizeof(uint16_t);
+        S.reserve(Scratch::rounded(up_bytes) + Scratch::rounded(256) + 6 * Scratch::rounded(n * 4) +
+                  2 * Scratch::rounded((K + 1) * 4) + Scratch::rounded((grid_for(K + 1, SCAN_TILE) + 1) * 4) +
+                  Scratch::rounded((size_t)recw * n * 8) + Scratch::rounded((size_t)items_cap * sizeof(BigItem)));
+        char* d_up = S.alloc<char>(up_bytes);
+        Plan* d_plan = (Plan*)d_up;
+        TabEntry* d_tab = (TabEntry*)(d_up + up_plan);
+        uint16_t* d_tasks = (uint16_t*)(d_up + up_plan + up_tab);
         char* misc = S.alloc<char>(256);
         int* d_err = (int*)misc;
         unsigned long long* d_m = (unsigned long long*)(misc + 16);
@@ -788,11 +868,23 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         uint32_t* bsum = S.alloc<uint32_t>(grid_for(K + 1, SCAN_TILE) + 1);
         uint32_t* sid = S.alloc<uint32_t>(n);
         uint32_t* skey = S.alloc<uint32_t>(n);
-        const int recw = d == 1 ? 2 : (d <= 3 ? 4 : 6);
         double* rec = S.alloc<double>((size_t)recw * n);
-        GCHECK(cudaMemcpyAsync(d_plan, &hp.p, sizeof(Plan), cudaMemcpyHostToDevice, st));
-        GCHECK(cudaMemcpyAsync(d_tab, hp.tab.data(), hp.tab.size() * sizeof(TabEntry), cudaMemcpyHostToDevice, st));
-        GCHECK(cudaMemcpyAsync(d_tasks, hp.tasks.data(), hp.tasks.size() * sizeof(uint16_t), cudaMemcpyHostToDevice, st));
+        BigItem* items = S.alloc<BigItem>(items_cap);
+        // plan, bound table and task lists in one upload from page-locked staging; the staging
+        // tail receives the status block at the end
+        char* stage = PE.staging(up_bytes + 256);
+        char* hmisc_pinned = stage ? stage + up_bytes : nullptr;
+        if (stage) {
+            std::memcpy(stage, &hp.p, sizeof(Plan));
+            std::memcpy(stage + up_plan, hp.tab.data(), hp.tab.size() * sizeof(TabEntry));
+            std::memcpy(stage + up_plan + up_tab, hp.tasks.data(), hp.tasks.size() * sizeof(uint16_t));
+            GCHECK(cudaMemcpyAsync(d_up, stage, up_bytes, cudaMemcpyHostToDevice, st));
+        } else {
+            GCHECK(cudaMemcpyAsync(d_plan, &hp.p, sizeof(Plan), cudaMemcpyHostToDevice, st));
+            GCHECK(cudaMemcpyAsync(d_tab, hp.tab.data(), hp.tab.size() * sizeof(TabEntry), cudaMemcpyHostToDevice, st));
+            GCHECK(cudaMemcpyAsync(d_tasks, hp.tasks.data(), hp.tasks.size() * sizeof(uint16_t),
+                                   cudaMemcpyHostToDevice, st));
+        }
         GCHECK(cudaMemsetAsync(misc, 0, 256, st));
         PE.record(1, st);
         switch (d) {
@@ -821,8 +913,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         a.nitems = (unsigned int*)(misc + 28);
         a.stats = stats_out ? d_cnt : nullptr;
         a.err = d_err;
-        unsigned int items_cap = std::max<unsigned int>(1u << 18, n32 / 2);
-        a.items = S.alloc<BigItem>(items_cap);
+        a.items = items;
         a.items_cap = items_cap;
         a.nP = K + 1;
         a.ntab = (unsigned)hp.tab.size();
@@ -835,7 +926,8 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         a.dev_flags = 0;
         if (const char* e = getenv("GIRG_DEV_FLAGS")) a.dev_flags = (unsigned)atoi(e);
         PE.record(2, st);
-        char hmisc[256];
+        char hmisc_local[256];
+        char* hmisc = hmisc_pinned ? hmisc_pinned : hmisc_local;
         for (int attempt = 0;; ++attempt) {
             switch (d) {
                 case 1: launch_sample<1>(a, scheme, st); break;
@@ -1235,6 +1327,75 @@ extern "C" int girg_edges_host(const double* w_host, const double* x_host, uint6
     } catch (...) {
         return GIRG_ENOMEM;
     }
+}
+
+// Batched small graphs: each graph is one unchanged edges_impl pipeline
+// (two host synchronisations: the weight statistics for the plan, the edge count); a pool of
+// native host threads, each with its own stream, runs them concurrently so that one graph's
+// host-side planning and synchronisations overlap other graphs' kernels on the 148 SMs.
+extern "C" int girg_edges_batch(int B, const double* const* w_dev, const double* const* x_dev, uint64_t n, int d,
+                                double T, const double* kappa, const uint64_t* seed, uint32_t* const* edges_dev,
+                                const uint64_t* cap, uint64_t* m_out, int* status_out, int nstreams, void* stream)
+{
+    if (B < 1 || !w_dev || !x_dev || !kappa || !seed || !edges_dev || !cap || !m_out) return GIRG_EINVAL;
+    if (n == 0 || n >= (1ull << 32) || d < 1 || d > 5 || !(T >= 0.0 && T < 1.0)) return GIRG_EINVAL;
+    for (int g = 0; g < B; ++g)  // per-graph arguments checked before any work is queued
+        if (!w_dev[g] || !x_dev[g] || (cap[g] && !edges_dev[g]) || !(kappa[g] > 0.0) || !std::isfinite(kappa[g]))
+            return GIRG_EINVAL;
+    const int nt = std::max(1, std::min(B, nstreams > 0 ? nstreams : 8));
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return map_cuda(cudaGetLastError());
+    std::vector<cudaStream_t> ss(nt, nullptr);
+    std::vector<cudaEvent_t> ev(nt + 1, nullptr);
+    std::vector<int> status(B, GIRG_OK);
+    auto cleanup = [&]() {
+        for (cudaStream_t s : ss)
+            if (s) cudaStreamDestroy(s);
+        for (cudaEvent_t e : ev)
+            if (e) cudaEventDestroy(e);
+    };
+    try {
+        for (int k = 0; k <= nt; ++k) GCHECK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+        GCHECK(cudaEventRecord(ev[nt], st));  // the batch starts after the caller's queued work
+        for (int k = 0; k < nt; ++k) {
+            GCHECK(cudaStreamCreateWithFlags(&ss[k], cudaStreamNonBlocking));
+            GCHECK(cudaStreamWaitEvent(ss[k], ev[nt], 0));
+        }
+    } catch (const CudaFail& f) {
+        cleanup();
+        return map_cuda(f.e);
+    }
+    std::atomic<int> next{0};
+    auto worker = [&](int k) {
+        if (cudaSetDevice(dev) != cudaSuccess) {
+            for (int g; (g = next.fetch_add(1)) < B;) status[g] = GIRG_ECUDA;
+            return;
+        }
+        for (int g; (g = next.fetch_add(1)) < B;) {
+            uint64_t m = 0;
+            status[g] = edges_impl(w_dev[g], x_dev[g], n, d, T, kappa[g], seed[g], 0, 0, 1, SCHEME_MERGED,
+                                   edges_dev[g], cap[g], &m, nullptr, ss[k]);
+            m_out[g] = m;
+        }
+        cudaEventRecord(ev[k], ss[k]);
+    };
+    {
+        std::vector<std::thread> pool;
+        for (int k = 1; k < nt; ++k) pool.emplace_back(worker, k);
+        worker(0);
+        for (std::thread& t : pool) t.join();
+    }
+    int rc = GIRG_OK;
+    for (int k = 0; k < nt; ++k)
+        if (cudaStreamWaitEvent(st, ev[k], 0) != cudaSuccess && rc == GIRG_OK) rc = GIRG_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess && rc == GIRG_OK) rc = GIRG_ECUDA;
+    cleanup();
+    for (int g = 0; g < B; ++g) {
+        if (status_out) status_out[g] = status[g];
+        if (rc == GIRG_OK && status[g] != GIRG_OK) rc = status[g];
+    }
+    return rc;
 }
 
 extern "C" const char* girg_strerror(int status)

@@ -74,6 +74,16 @@ def test_argument_validation_before_launch(girg):
     assert L.girg_scale_weights(1234, 10, 9.0, 1, 0.5, 2.5, C.byref(k), None) == girg.EINVAL  # avg_deg >= n-1
     assert L.girg_scale_weights(1234, 10, 1.0, 1, 0.5, 2.0, C.byref(k), None) == girg.EINVAL  # beta
     assert L.girg_edges_host(None, 1234, 10, 1, 0.5, 1.0, 1, 1234, 10, C.byref(m), None) == girg.EINVAL
+    P2, D2, U2 = C.c_void_p * 2, C.c_double * 2, C.c_uint64 * 2
+    ptr, kap, sd, cp, mo = P2(1234, 1234), D2(1.0, 1.0), U2(1, 2), U2(10, 10), U2()
+    assert L.girg_edges_batch(0, ptr, ptr, 10, 1, 0.5, kap, sd, ptr, cp, mo, None, 0, None) == girg.EINVAL  # B
+    assert L.girg_edges_batch(2, None, ptr, 10, 1, 0.5, kap, sd, ptr, cp, mo, None, 0, None) == girg.EINVAL
+    assert L.girg_edges_batch(2, ptr, ptr, 10, 1, 1.0, kap, sd, ptr, cp, mo, None, 0, None) == girg.EINVAL  # T
+    assert L.girg_edges_batch(2, ptr, ptr, 10, 6, 0.5, kap, sd, ptr, cp, mo, None, 0, None) == girg.EINVAL  # d
+    assert L.girg_edges_batch(2, ptr, ptr, 10, 1, 0.5, D2(1.0, -1.0), sd, ptr, cp, mo, None, 0,
+                              None) == girg.EINVAL  # one bad kappa
+    assert L.girg_edges_batch(2, P2(1234, None), ptr, 10, 1, 0.5, kap, sd, ptr, cp, mo, None, 0,
+                              None) == girg.EINVAL  # one null weight pointer
     for bad in (girg.Options(7, 0, 0, 1), girg.Options(-1, 0, 0, 1), girg.Options(girg.SCHEME_EVENT, 0, 1, 1)):
         assert L.girg_edges_ex(1234, 1234, 10, 2, 0.5, 1.0, 1, C.byref(bad), 1234, 10, C.byref(m), None,
                                None) == girg.EINVAL  # unknown scheme / empty block range

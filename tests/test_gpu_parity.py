@@ -260,3 +260,47 @@ def test_host_buffer_call_matches_device_call():
     m = girg.edges_host(torch.from_numpy(w), torch.from_numpy(x), d, T, kappa, 5, pageable)
     assert m == len(ref)
     assert np.array_equal(girg.edge_keys(pageable[:m]).numpy().astype(np.uint64), ref)
+
+
+# ------------------------------------------------------- batched small graphs (NEXT-4) ----
+@pytest.mark.parametrize("d,T", [(1, 0.0), (2, 0.5), (3, 0.8)])
+def test_batch_equals_single_calls_and_oracle(d, T):
+    """girg_edges_batch: every graph of the batch equals its own girg_edges call (and, for two of
+    them, the oracle), with mixed seeds and kappas, more graphs than streams, and one graph whose
+    capacity is too small (ECAPACITY for that graph only, re-issued by the binding)."""
+    n, beta, B = 5003, 2.5, 7
+    ws, xs, kap, seeds = [], [], [], []
+    for g in range(B):
+        w, x = synth_inputs(n, d, beta, 100 + 7 * g + d)
+        ws.append(w)
+        xs.append(x)
+        kap.append(O.scale_weights(w, 4.0 + g, d, T, beta))
+        seeds.append(1000 + g)
+    caps = [16 * n + 1024] * B
+    caps[3] = 5  # too small: the library reports the exact count, the binding re-issues graph 3
+    out = girg.edges_batch([dev(w) for w in ws], [dev(x) for x in xs], T, kap, seeds, caps=caps, nstreams=3)
+    assert len(out) == B
+    for g in range(B):
+        single = girg.edges(dev(ws[g]), dev(xs[g]), T, kap[g], seeds[g])
+        assert np.array_equal(gpu_keys(out[g]), gpu_keys(single)), g
+    for g in (0, 3):
+        eo, so = O.edges(ws[g], xs[g], d, T, kap[g], seeds[g], with_stats=True)
+        assert so["nt1"] + so["nt2acc"] + so["nt2jump"] == 0, so
+        assert np.array_equal(gpu_keys(out[g]), O.sort_edges(eo)), g
+
+
+def test_batch_single_graph_and_status():
+    """B = 1 through the raw ABI: status_out and m_out per graph, and a capacity failure."""
+    import ctypes as C
+    n, d, T, beta = 2000, 2, 0.3, 2.4
+    w, x = synth_inputs(n, d, beta, 5)
+    kappa = O.scale_weights(w, 6.0, d, T, beta)
+    wd, xd = dev(w), dev(x)
+    buf = torch.empty((4, 2), dtype=torch.int32, device="cuda")
+    P1 = C.c_void_p * 1
+    mo, so = (C.c_uint64 * 1)(), (C.c_int * 1)()
+    rc = girg._lib.girg_edges_batch(1, P1(wd.data_ptr()), P1(xd.data_ptr()), n, d, T, (C.c_double * 1)(kappa),
+                                    (C.c_uint64 * 1)(9), P1(buf.data_ptr()), (C.c_uint64 * 1)(4), mo, so, 0, None)
+    ref = girg.edges(wd, xd, T, kappa, 9)
+    assert rc == girg.ECAPACITY and so[0] == girg.ECAPACITY
+    assert mo[0] == ref.shape[0] > 4
