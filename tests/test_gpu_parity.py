@@ -304,3 +304,16 @@ def test_batch_single_graph_and_status():
     ref = girg.edges(wd, xd, T, kappa, 9)
     assert rc == girg.ECAPACITY and so[0] == girg.ECAPACITY
     assert mo[0] == ref.shape[0] > 4
+
+
+@pytest.mark.parametrize("d", [1, 2, 3])
+@pytest.mark.parametrize("T,beta", [(0.99, 2.5), (0.02, 2.5), (0.5, 2.05), (0.0, 2.05), (0.7, 6.0)])
+def test_parameter_extremes(d, T, beta):
+    """Temperatures near 1 (flat p, pbar near 1 on coarse levels) and near 0 (p close to a step),
+    beta near 2 (huge hub weights, many layers) and a light tail (beta = 6: few layers)."""
+    n = 20_000
+    w, x = synth_inputs(n, d, beta, 300 + d)
+    kappa = O.scale_weights(w, 10.0, d, T, beta)
+    g, st, so = assert_parity(w, x, d, T, kappa, 11)
+    if beta >= 2.5:  # degree near target (for beta ~ 2 the realised degree is dominated by a few hubs)
+        assert abs(2 * len(g) / n - 10.0) < 2.0
