@@ -924,6 +924,12 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         if (const char* e = getenv("GIRG_ITEM_WORK")) a.item_work = strtoull(e, nullptr, 10);
         a.wprof = nullptr;
         a.dev_flags = 0;
+        a.T = hp.p.T;
+        a.s = hp.p.s;
+        a.invT = hp.p.invT;
+        a.sl = hp.p.sl;
+        a.blo = hp.p.blo;
+        a.bhi = hp.p.bhi;
         if (const char* e = getenv("GIRG_DEV_FLAGS")) a.dev_flags = (unsigned)atoi(e);
         PE.record(2, st);
         char hmisc_local[256];

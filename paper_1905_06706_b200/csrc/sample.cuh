@@ -151,6 +151,11 @@ struct SampleArgs {
     unsigned long long big_work, item_work;  // job split thresholds (BIG_WORK / ITEM_WORK by default)
     unsigned long long* wprof;               // optional per-warp profile: cycles, jobs, iterations, lane steps
     unsigned dev_flags;                      // development (-DGIRG_PROFILE builds): 1 = set up jobs, skip units
+    // copies of Plan scalars read in the hot loops: kernel parameters are instruction operands
+    // (constant bank), a Plan field is a global load that register pressure makes the compiler repeat
+    double T, s, invT;
+    int sl;
+    unsigned long long blo, bhi;
 };
 
 struct TaskDesc {
@@ -444,9 +449,9 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
             if (e < nsub) {
                 ok = S.achild[e + 1] > S.achild[e];
                 const uint32_t A = (t.Cpar << t.cs) + (uint32_t)e;
-                const unsigned long long b = t.l >= pl->sl ? ((unsigned long long)A >> (D * (t.l - pl->sl)))
-                                                           : ((unsigned long long)A << (D * (pl->sl - t.l)));
-                ok = ok && b >= pl->blo && b < pl->bhi;
+                const unsigned long long b = t.l >= a.sl ? ((unsigned long long)A >> (D * (t.l - a.sl)))
+                                                         : ((unsigned long long)A << (D * (a.sl - t.l)));
+                ok = ok && b >= a.blo && b < a.bhi;
             }
             const unsigned bm = __ballot_sync(FULL, ok);
             const int rank = cnt + __popc(bm & ((1u << lane) - 1u));
@@ -1129,10 +1134,9 @@ struct ItemSource {
 template <int D, int SCHEME, bool STATS, class Src>
 __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src& src, Counters& C)
 {
-    const Plan* pl = a.pl;
     const unsigned lane = lane_id();
-    const bool T0 = pl->T == 0.0;
-    const double s_ = pl->s, invT = pl->invT;
+    const bool T0 = a.T == 0.0;
+    const double s_ = a.s, invT = a.invT;
 #ifdef GIRG_PROFILE
     const long long t_start = clock64();
     unsigned long long n_jobs = 0, n_iter = 0, n_steps = 0;
