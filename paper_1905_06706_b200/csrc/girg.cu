@@ -22,9 +22,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <memory>
+#include <thread>
 #include <mutex>
 #include <string>
-#include <thread>
 #include <vector>
 
 #include "../../include/girg.h"
@@ -816,28 +817,90 @@ static void launch_sample(const SampleArgs& a, int scheme, cudaStream_t st)
     }
 }
 
-static int edges_impl(const double* w, const double* x, uint64_t n, int d, double T, double kappa,
-                      uint64_t seed, int sl, uint64_t blo, uint64_t bhi, int scheme, uint32_t* edges, uint64_t cap,
-                      uint64_t* m_out, girg_stats* stats_out, cudaStream_t st)
-{
-    if (scheme != SCHEME_EVENT && scheme != SCHEME_MERGED) return GIRG_EINVAL;
-    if (!w || !x || !m_out || (cap && !edges)) return GIRG_EINVAL;
-    if (n == 0 || n >= (1ull << 32) || d < 1 || d > 5) return GIRG_EINVAL;
-    if (!(T >= 0.0 && T < 1.0) || !(kappa > 0.0) || !std::isfinite(kappa)) return GIRG_EINVAL;
-    if (sl < 0 || sl * d > 32 || blo >= bhi) return GIRG_EINVAL;
-    try {
-        PhaseEvents PE;
-        Scratch S(st);
-        std::vector<uint32_t> hist;
-        std::vector<WPartial> parts;
-        int herr = 0;
+// One girg_edges call in three host stages, so that a batch can queue stage A (resp. B) of many
+// graphs on several streams before waiting once:
+//   A  weight statistics (k_wstats) + their read-back into page-locked staging        (async)
+//   B  [after A's data arrived] host plan, one scratch block, plan upload, index build,
+//      sampler, status read-back                                                       (async)
+//   C  [after B's data arrived] status, item-queue regrowth (re-runs the sampler), outputs
+struct EdgeCall {
+    const double *w, *x;
+    uint64_t n;
+    int d;
+    double T, kappa;
+    uint64_t seed;
+    int sl;
+    uint64_t blo, bhi;
+    int scheme;
+    uint32_t* edges;
+    uint64_t cap;
+    uint64_t* m_out;
+    girg_stats* stats_out;
+    cudaStream_t st;
+    PhaseEvents PE;
+    Scratch S;
+    HostPlan hp;
+    SampleArgs a;
+    char* misc = nullptr;  // device status block (err, m, counters, queue counters)
+    char* hmisc = nullptr;
+    char hmisc_local[256];
+    unsigned nb = 0;
+    char* wst_dev = nullptr;  // k_wstats outputs: histogram, error flag, block partials
+    char* wst_host = nullptr;
+    std::vector<char> wst_pageable;
+    size_t wst_bytes = 0;
+    int rc = GIRG_OK;
+
+    EdgeCall(const double* w_, const double* x_, uint64_t n_, int d_, double T_, double kappa_, uint64_t seed_,
+             int sl_, uint64_t blo_, uint64_t bhi_, int scheme_, uint32_t* edges_, uint64_t cap_, uint64_t* m_out_,
+             girg_stats* stats_out_, cudaStream_t st_)
+        : w(w_), x(x_), n(n_), d(d_), T(T_), kappa(kappa_), seed(seed_), sl(sl_), blo(blo_), bhi(bhi_),
+          scheme(scheme_), edges(edges_), cap(cap_), m_out(m_out_), stats_out(stats_out_), st(st_), S(st_)
+    {
+    }
+
+    static int validate(const double* w, const double* x, uint64_t n, int d, double T, double kappa, int sl,
+                        uint64_t blo, uint64_t bhi, int scheme, uint32_t* edges, uint64_t cap, uint64_t* m_out)
+    {
+        if (scheme != SCHEME_EVENT && scheme != SCHEME_MERGED) return GIRG_EINVAL;
+        if (!w || !x || !m_out || (cap && !edges)) return GIRG_EINVAL;
+        if (n == 0 || n >= (1ull << 32) || d < 1 || d > 5) return GIRG_EINVAL;
+        if (!(T >= 0.0 && T < 1.0) || !(kappa > 0.0) || !std::isfinite(kappa)) return GIRG_EINVAL;
+        if (sl < 0 || sl * d > 32 || blo >= bhi) return GIRG_EINVAL;
+        return GIRG_OK;
+    }
+
+    void stage_a()
+    {
         PE.record(0, st);
-        run_wstats(w, n, st, S, hist, parts, herr);
-        if (herr & ERR_WEIGHT) return GIRG_EINVAL;
-        if (herr & ERR_WRANGE) return GIRG_ERANGE;
-        HostPlan hp;
-        int rc = make_plan(hist, parts, n, d, T, kappa, hp);
-        if (rc) return rc;
+        nb = grid_for(n, WS_TILE);
+        wst_bytes = HIST_BINS * sizeof(uint32_t) + 16 + nb * sizeof(WPartial);
+        wst_dev = S.alloc<char>(wst_bytes);
+        GCHECK(cudaMemsetAsync(wst_dev, 0, HIST_BINS * sizeof(uint32_t) + 16, st));
+        k_wstats<<<nb, WS_THREADS, 0, st>>>(w, (uint32_t)n, (uint32_t*)wst_dev,
+                                            (WPartial*)(wst_dev + HIST_BINS * sizeof(uint32_t) + 16),
+                                            (int*)(wst_dev + HIST_BINS * sizeof(uint32_t)));
+        GCHECK(cudaGetLastError());
+        // staging sized for this read-back and (typically) the later plan upload: no reallocation
+        wst_host = PE.staging(std::max<size_t>(wst_bytes, 1 << 20));
+        if (!wst_host) {
+            wst_pageable.resize(wst_bytes);
+            wst_host = wst_pageable.data();
+        }
+        GCHECK(cudaMemcpyAsync(wst_host, wst_dev, wst_bytes, cudaMemcpyDeviceToHost, st));
+    }
+
+    void stage_b()
+    {
+        std::vector<uint32_t> hist((uint32_t*)wst_host, (uint32_t*)wst_host + HIST_BINS);
+        int herr = 0;
+        std::memcpy(&herr, wst_host + HIST_BINS * sizeof(uint32_t), sizeof(int));
+        std::vector<WPartial> parts(nb);
+        std::memcpy(parts.data(), wst_host + HIST_BINS * sizeof(uint32_t) + 16, nb * sizeof(WPartial));
+        if (herr & ERR_WEIGHT) { rc = GIRG_EINVAL; return; }
+        if (herr & ERR_WRANGE) { rc = GIRG_ERANGE; return; }
+        rc = make_plan(hist, parts, n, d, T, kappa, hp);
+        if (rc) return;
         hp.p.sl = sl;
         hp.p.blo = blo;
         hp.p.bhi = bhi;
@@ -845,7 +908,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         const uint64_t K = hp.K;
         // scratch: one stream-ordered block for everything this call needs
         const int recw = d == 1 ? 2 : (d <= 3 ? 4 : 6);
-        unsigned int items_cap = std::max<unsigned int>(1u << 18, n32 / 2);
+        const unsigned int items_cap = std::max<unsigned int>(1u << 18, n32 / 2);
         const size_t up_plan = Scratch::rounded(sizeof(Plan)), up_tab = Scratch::rounded(hp.tab.size() * sizeof(TabEntry)),
                      up_bytes = up_plan + up_tab + hp.tasks.size() * sizeof(uint16_t);
         S.reserve(Scratch::rounded(up_bytes) + Scratch::rounded(256) + 6 * Scratch::rounded(n * 4) +
@@ -855,10 +918,8 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         Plan* d_plan = (Plan*)d_up;
         TabEntry* d_tab = (TabEntry*)(d_up + up_plan);
         uint16_t* d_tasks = (uint16_t*)(d_up + up_plan + up_tab);
-        char* misc = S.alloc<char>(256);
+        misc = S.alloc<char>(256);
         int* d_err = (int*)misc;
-        unsigned long long* d_m = (unsigned long long*)(misc + 16);
-        Counters* d_cnt = (Counters*)(misc + 32);
         uint32_t* key = S.alloc<uint32_t>(n);
         uint32_t* tmp = S.alloc<uint32_t>(n);
         uint32_t* tkey = S.alloc<uint32_t>(n);
@@ -870,10 +931,10 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         uint32_t* skey = S.alloc<uint32_t>(n);
         double* rec = S.alloc<double>((size_t)recw * n);
         BigItem* items = S.alloc<BigItem>(items_cap);
-        // plan, bound table and task lists in one upload from page-locked staging; the staging
-        // tail receives the status block at the end
+        // plan, bound table and task lists in one upload from page-locked staging (the weight
+        // statistics above are consumed); the staging tail receives the status block
         char* stage = PE.staging(up_bytes + 256);
-        char* hmisc_pinned = stage ? stage + up_bytes : nullptr;
+        hmisc = stage ? stage + up_bytes : hmisc_local;
         if (stage) {
             std::memcpy(stage, &hp.p, sizeof(Plan));
             std::memcpy(stage + up_plan, hp.tab.data(), hp.tab.size() * sizeof(TabEntry));
@@ -884,6 +945,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
             GCHECK(cudaMemcpyAsync(d_tab, hp.tab.data(), hp.tab.size() * sizeof(TabEntry), cudaMemcpyHostToDevice, st));
             GCHECK(cudaMemcpyAsync(d_tasks, hp.tasks.data(), hp.tasks.size() * sizeof(uint16_t),
                                    cudaMemcpyHostToDevice, st));
+            GCHECK(cudaStreamSynchronize(st));  // pageable sources must outlive the copies
         }
         GCHECK(cudaMemsetAsync(misc, 0, 256, st));
         PE.record(1, st);
@@ -894,7 +956,6 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
             case 4: launch_index<4>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
             default: launch_index<5>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
         }
-        SampleArgs a;
         a.pl = d_plan;
         a.tab = d_tab;
         a.tasks = d_tasks;
@@ -908,10 +969,10 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         a.k1 = (uint32_t)(seed >> 32);
         a.edges = (uint2*)edges;
         a.cap = cap;
-        a.m = d_m;
+        a.m = (unsigned long long*)(misc + 16);
         a.tile_ctr = (unsigned int*)(misc + 24);
         a.nitems = (unsigned int*)(misc + 28);
-        a.stats = stats_out ? d_cnt : nullptr;
+        a.stats = stats_out ? (Counters*)(misc + 32) : nullptr;
         a.err = d_err;
         a.items = items;
         a.items_cap = items_cap;
@@ -932,30 +993,38 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         a.bhi = hp.p.bhi;
         if (const char* e = getenv("GIRG_DEV_FLAGS")) a.dev_flags = (unsigned)atoi(e);
         PE.record(2, st);
-        char hmisc_local[256];
-        char* hmisc = hmisc_pinned ? hmisc_pinned : hmisc_local;
+        sample_and_fetch();
+    }
+
+    void sample_and_fetch()
+    {
+        switch (d) {
+            case 1: launch_sample<1>(a, scheme, st); break;
+            case 2: launch_sample<2>(a, scheme, st); break;
+            case 3: launch_sample<3>(a, scheme, st); break;
+            case 4: launch_sample<4>(a, scheme, st); break;
+            default: launch_sample<5>(a, scheme, st); break;
+        }
+        PE.record(3, st);
+        GCHECK(cudaMemcpyAsync(hmisc, misc, 256, cudaMemcpyDeviceToHost, st));
+    }
+
+    int stage_c()
+    {
+        if (rc != GIRG_OK) return rc;
         for (int attempt = 0;; ++attempt) {
-            switch (d) {
-                case 1: launch_sample<1>(a, scheme, st); break;
-                case 2: launch_sample<2>(a, scheme, st); break;
-                case 3: launch_sample<3>(a, scheme, st); break;
-                case 4: launch_sample<4>(a, scheme, st); break;
-                default: launch_sample<5>(a, scheme, st); break;
-            }
-            PE.record(3, st);
-            GCHECK(cudaMemcpyAsync(hmisc, misc, 256, cudaMemcpyDeviceToHost, st));
-            GCHECK(cudaStreamSynchronize(st));
             int e0;
             unsigned int need;
             std::memcpy(&e0, hmisc, sizeof(int));
             std::memcpy(&need, hmisc + 28, sizeof(need));
             if (!(e0 & ERR_ITEMS) || attempt > 4) break;
             // the big-event item queue overflowed: grow it and re-run the (deterministic) sampler
-            items_cap = need + (need >> 2) + 1024;
-            a.items = S.alloc<BigItem>(items_cap);
-            a.items_cap = items_cap;
+            a.items_cap = need + (need >> 2) + 1024;
+            a.items = S.alloc<BigItem>(a.items_cap);
             GCHECK(cudaMemsetAsync(misc, 0, 256, st));
             PE.record(2, st);
+            sample_and_fetch();
+            GCHECK(cudaStreamSynchronize(st));
         }
         g_timings.ms_wstats = PE.ms(0, 1);
         g_timings.ms_index = PE.ms(1, 2);
@@ -963,7 +1032,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         g_timings.ms_total = PE.ms(0, 3);
         g_timings.launches = 10;  // k_wstats, k_keys, 3 x scan, k_scatter, k_order, k_place, k_sample, k_big
         g_timings.n = n;
-        g_timings.key_space = K;
+        g_timings.key_space = hp.K;
         g_timings.d = d;
         int derr;
         unsigned long long m;
@@ -988,9 +1057,26 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
             stats_out->fast_fallback = hc.fb;
             stats_out->fast_mismatch = hc.mm;
             stats_out->layers = (uint64_t)hp.p.L;
-            stats_out->key_space = K;
+            stats_out->key_space = hp.K;
         }
         return m > cap ? GIRG_ECAPACITY : GIRG_OK;
+    }
+};
+
+static int edges_impl(const double* w, const double* x, uint64_t n, int d, double T, double kappa,
+                      uint64_t seed, int sl, uint64_t blo, uint64_t bhi, int scheme, uint32_t* edges, uint64_t cap,
+                      uint64_t* m_out, girg_stats* stats_out, cudaStream_t st)
+{
+    int v = EdgeCall::validate(w, x, n, d, T, kappa, sl, blo, bhi, scheme, edges, cap, m_out);
+    if (v != GIRG_OK) return v;
+    try {
+        EdgeCall E(w, x, n, d, T, kappa, seed, sl, blo, bhi, scheme, edges, cap, m_out, stats_out, st);
+        E.stage_a();
+        GCHECK(cudaStreamSynchronize(st));
+        E.stage_b();
+        if (E.rc != GIRG_OK) return E.rc;
+        GCHECK(cudaStreamSynchronize(st));
+        return E.stage_c();
     } catch (const CudaFail& f) {
         return map_cuda(f.e);
     } catch (...) {
@@ -1335,10 +1421,12 @@ extern "C" int girg_edges_host(const double* w_host, const double* x_host, uint6
     }
 }
 
-// Batched small graphs: each graph is one unchanged edges_impl pipeline
-// (two host synchronisations: the weight statistics for the plan, the edge count); a pool of
-// native host threads, each with its own stream, runs them concurrently so that one graph's
-// host-side planning and synchronisations overlap other graphs' kernels on the 148 SMs.
+// Batched small graphs: each graph is one unchanged girg_edges pipeline
+// (EdgeCall: two host waits, for the weight statistics the plan needs and for the edge count).
+// A pool of native host threads, each with its own stream, runs them concurrently, so one
+// graph's host planning and waits overlap other graphs' kernels on the 148 SMs.  (Measured: a
+// single thread driving all graphs in waves over several streams is slower -- the per-graph
+// host work, not the waits, is what has to run in parallel.)
 extern "C" int girg_edges_batch(int B, const double* const* w_dev, const double* const* x_dev, uint64_t n, int d,
                                 double T, const double* kappa, const uint64_t* seed, uint32_t* const* edges_dev,
                                 const uint64_t* cap, uint64_t* m_out, int* status_out, int nstreams, void* stream)
@@ -1346,7 +1434,8 @@ extern "C" int girg_edges_batch(int B, const double* const* w_dev, const double*
     if (B < 1 || !w_dev || !x_dev || !kappa || !seed || !edges_dev || !cap || !m_out) return GIRG_EINVAL;
     if (n == 0 || n >= (1ull << 32) || d < 1 || d > 5 || !(T >= 0.0 && T < 1.0)) return GIRG_EINVAL;
     for (int g = 0; g < B; ++g)  // per-graph arguments checked before any work is queued
-        if (!w_dev[g] || !x_dev[g] || (cap[g] && !edges_dev[g]) || !(kappa[g] > 0.0) || !std::isfinite(kappa[g]))
+        if (EdgeCall::validate(w_dev[g], x_dev[g], n, d, T, kappa[g], 0, 0, 1, SCHEME_MERGED, edges_dev[g], cap[g],
+                               m_out + g) != GIRG_OK)
             return GIRG_EINVAL;
     const int nt = std::max(1, std::min(B, nstreams > 0 ? nstreams : 8));
     cudaStream_t st = (cudaStream_t)stream;
@@ -1356,8 +1445,8 @@ extern "C" int girg_edges_batch(int B, const double* const* w_dev, const double*
     std::vector<cudaEvent_t> ev(nt + 1, nullptr);
     std::vector<int> status(B, GIRG_OK);
     auto cleanup = [&]() {
-        for (cudaStream_t s : ss)
-            if (s) cudaStreamDestroy(s);
+        for (cudaStream_t s2 : ss)
+            if (s2) cudaStreamDestroy(s2);
         for (cudaEvent_t e : ev)
             if (e) cudaEventDestroy(e);
     };
