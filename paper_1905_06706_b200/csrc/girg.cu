@@ -823,6 +823,8 @@ static void launch_sample(const SampleArgs& a, int scheme, cudaStream_t st)
 //   B  [after A's data arrived] host plan, one scratch block, plan upload, index build,
 //      sampler, status read-back                                                       (async)
 //   C  [after B's data arrived] status, item-queue regrowth (re-runs the sampler), outputs
+static_assert(32 + sizeof(Counters) <= 128, "status block layout: counters end before the item counter");
+
 struct EdgeCall {
     const double *w, *x;
     uint64_t n;
@@ -972,6 +974,7 @@ struct EdgeCall {
         a.m = (unsigned long long*)(misc + 16);
         a.tile_ctr = (unsigned int*)(misc + 24);
         a.nitems = (unsigned int*)(misc + 28);
+        a.item_ctr = (unsigned int*)(misc + 128);  // after the counters (32 + sizeof(Counters) <= 128)
         a.stats = stats_out ? (Counters*)(misc + 32) : nullptr;
         a.err = d_err;
         a.items = items;

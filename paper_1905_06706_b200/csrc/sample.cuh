@@ -143,6 +143,7 @@ struct SampleArgs {
     unsigned int* tile_ctr;
     BigItem* items;
     unsigned int* nitems;
+    unsigned int* item_ctr;  // k_big's dynamic item counter (zeroed with the status block)
     unsigned int items_cap;
     Counters* stats;
     int* err;
@@ -1092,20 +1093,24 @@ struct TileSource {
 // k_big: warps pull queued items (unit ranges of big jobs)
 template <int D, int SCHEME, bool STATS>
 struct ItemSource {
-    unsigned k, nit, stride;
+    unsigned nit;
     __device__ __noinline__ bool next(const SampleArgs& a, SlotT<D>& S, unsigned long long& lo,
                                          unsigned long long& hi, Counters& C)
     {
         for (;;) {
+            // dynamic assignment (one atomic per item): the kernel's tail is one item, not the
+            // spread of per-warp sums of a static stride
+            unsigned k = 0;
+            if (lane_id() == 0) k = atomicAdd(a.item_ctr, 1u);
+            k = __shfl_sync(FULL, k, 0);
             if (k >= nit) return false;
             const BigItem it = a.items[k];
-            k += stride;
             const TaskDesc t = make_task<D>(it.i, it.task, it.Cpar);
             const JobSetup js = setup_any<D, SCHEME>(a, S, t, it.batch);  // sequences were counted by the job that queued it
             (void)C;
 #ifdef GIRG_DEBUG
             if (js.U < it.hi && lane_id() == 0)
-                printf("k_big item %u: job U %llu < item hi %llu (i %d task %x Cpar %u batch %d nchild %d)\n", k - stride,
+                printf("k_big item %u: job U %llu < item hi %llu (i %d task %x Cpar %u batch %d nchild %d)\n", k,
                        js.U, it.hi, it.i, it.task, it.Cpar, it.batch, js.nchild);
 #endif
             if (js.U < it.hi) {
@@ -1382,8 +1387,6 @@ __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_big(SampleAr
     // an overflowing push skipped its whole reservation, so [0, cap) may hold unwritten items:
     // on overflow do nothing (the host grows the queue and re-runs the sampler)
     src.nit = (*a.err & ERR_ITEMS) ? 0u : min(*a.nitems, a.items_cap);
-    src.stride = gridDim.x * Geo<D>::WPB;
-    src.k = blockIdx.x * Geo<D>::WPB + (threadIdx.x >> 5);
     engine<D, SCHEME, STATS>(a, W, src, C);
     flush_counters<STATS>(a, C);
 }
