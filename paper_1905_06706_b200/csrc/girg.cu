@@ -982,8 +982,8 @@ struct EdgeCall {
         a.nP = K + 1;
         a.ntab = (unsigned)hp.tab.size();
         a.ntasks = (unsigned)hp.tasks.size();
-        a.big_work = big_work(d);
-        a.item_work = item_work(d);
+        a.big_work = big_work(d, n);
+        a.item_work = item_work(d, n);
         if (const char* e = getenv("GIRG_BIG_WORK")) a.big_work = strtoull(e, nullptr, 10);
         if (const char* e = getenv("GIRG_ITEM_WORK")) a.item_work = strtoull(e, nullptr, 10);
         a.wprof = nullptr;

@@ -50,8 +50,14 @@ constexpr int SCHEME_EVENT = 0, SCHEME_MERGED = 1;
 #endif
 constexpr int EB = GIRG_EB;                      // staged edges per warp
 // weighted units (a chunk counts 8) above which a job is queued for k_big, and per queued item
-__host__ __device__ constexpr unsigned long long big_work(int d) { return d == 1 ? 512ull : (d == 2 ? 2048ull : 32768ull); }
-__host__ __device__ constexpr unsigned long long item_work(int d) { return d == 1 ? 256ull : (d == 2 ? 1024ull : 16384ull); }
+// Jobs with more units than big_work are queued for k_big in items of item_work units (B200
+// sweeps, profiles/r01/SUMMARY.md; d = 1 splits finer on small graphs, which have fewer jobs
+// per warp: C2 512 / 256 3.16 ms vs 1024 / 512 3.51 ms, C4 the other way round 25.1 vs 23.5 ms).
+__host__ __device__ constexpr unsigned long long big_work(int d, unsigned long long n)
+{
+    return d == 1 ? (n >= (1ull << 22) ? 1024ull : 512ull) : (d == 2 ? 1024ull : (d == 3 ? 16384ull : 32768ull));
+}
+__host__ __device__ constexpr unsigned long long item_work(int d, unsigned long long n) { return big_work(d, n) / 2; }
 constexpr int ERR_ITEMS = 16;
 constexpr unsigned FULL = 0xffffffffu;
 
