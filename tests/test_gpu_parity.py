@@ -317,3 +317,19 @@ def test_parameter_extremes(d, T, beta):
     g, st, so = assert_parity(w, x, d, T, kappa, 11)
     if beta >= 2.5:  # degree near target (for beta ~ 2 the realised degree is dominated by a few hubs)
         assert abs(2 * len(g) / n - 10.0) < 2.0
+
+
+def test_big_job_items_and_queue_regrowth(monkeypatch):
+    """Every job split into 1-unit k_big items (development thresholds GIRG_BIG_WORK /
+    GIRG_ITEM_WORK): far more items than the initial queue holds, so the library must grow the
+    queue and re-run the sampler; the edge set is unchanged (schedule independence)."""
+    n, d, T, beta = 20_000, 2, 0.6, 2.3
+    w, x = synth_inputs(n, d, beta, 77)
+    kappa = O.scale_weights(w, 12.0, d, T, beta)
+    ref, st0 = girg.edges(dev(w), dev(x), T, kappa, 5, stats=True)
+    monkeypatch.setenv("GIRG_BIG_WORK", "2")
+    monkeypatch.setenv("GIRG_ITEM_WORK", "1")
+    got, st1 = girg.edges(dev(w), dev(x), T, kappa, 5, stats=True)
+    assert np.array_equal(gpu_keys(got), gpu_keys(ref))
+    assert st1["landings"] == st0["landings"] and st1["cand1"] == st0["cand1"]
+    assert st1["cand1"] + st1["chunks"] > (1 << 18)  # more 1-unit items than the initial queue
