@@ -48,7 +48,9 @@ constexpr int SCHEME_EVENT = 0, SCHEME_MERGED = 1;
 #ifndef GIRG_EB
 #define GIRG_EB 128
 #endif
-constexpr int EB = GIRG_EB;                      // staged edges per warp
+#ifndef GIRG_EB3
+#define GIRG_EB3 64
+#endif
 // weighted units (a chunk counts 8) above which a job is queued for k_big, and per queued item
 // Jobs with more units than big_work are queued for k_big in items of item_work units (B200
 // sweeps, profiles/r01/SUMMARY.md; d = 1 splits finer on small graphs, which have fewer jobs
@@ -66,7 +68,10 @@ constexpr unsigned FULL = 0xffffffffu;
 //   GIRG_G1      d = 1 task height: a job covers the 2^G1 level-l cells below one task cell
 //   GIRG_NSLOT1  d = 1 job slots per warp;  GIRG_MINB1  d = 1 resident blocks per SM
 //   GIRG_WPB3    d = 3 warps per block;     GIRG_NSLOT3 / GIRG_MINB3  d = 3 slots / blocks per SM
-//   GIRG_EB      staged edges per warp
+//   GIRG_EB / GIRG_EB3  staged edges per warp (d != 3 / d = 3);  GIRG_MINB2  d = 2 blocks per SM
+//   (d = 3: 5 blocks of 4 warps need <= 96 registers AND <= 45 KB of shared memory per block,
+//    hence the 64-entry staging buffer: 164 vs 176 ms on C5; 5 blocks without it stay at 4
+//    resident blocks with the 96-register cap and run slower, 186 ms)
 // GIRG_PROFILE adds per-warp cycle / job / iteration counters (GIRG_WARP_PROFILE dumps them).
 #ifndef GIRG_G1
 #define GIRG_G1 4
@@ -83,8 +88,11 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef GIRG_NSLOT3
 #define GIRG_NSLOT3 2
 #endif
+#ifndef GIRG_MINB2
+#define GIRG_MINB2 4
+#endif
 #ifndef GIRG_MINB3
-#define GIRG_MINB3 4
+#define GIRG_MINB3 5
 #endif
 template <int D>
 struct Geo {
@@ -94,7 +102,8 @@ struct Geo {
     static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // lg = 1: all 2^d level-1 cells
     static constexpr int CB = D <= 3 ? NCH : (D == 4 ? 4 : 2);        // children per job (batch)
     static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? GIRG_WPB3 : 2);  // warps per block
-    static constexpr int MINB = D == 1 ? GIRG_MINB1 : (D == 2 ? 3 : (D == 3 ? GIRG_MINB3 : 1));  // resident blocks per SM
+    static constexpr int MINB = D == 1 ? GIRG_MINB1 : (D == 2 ? GIRG_MINB2 : (D == 3 ? GIRG_MINB3 : 1));  // resident blocks per SM
+    static constexpr int EB = D == 3 ? GIRG_EB3 : GIRG_EB;  // staged edges per warp (d = 3: small, so 5 blocks fit)
     static constexpr int NSLOT = D == 1 ? GIRG_NSLOT1 : (D == 2 ? 3 : (D == 3 ? GIRG_NSLOT3 : 2));  // job slots per warp
     static constexpr int RECW = D == 1 ? 2 : (D <= 3 ? 4 : 6);       // doubles per point record
 };
@@ -220,7 +229,7 @@ using SlotT = typename std::conditional<D == 1, Slot1, Slot<D>>::type;
 template <int D>
 struct WarpSmem {
     SlotT<D> slot[Geo<D>::NSLOT];
-    uint2 ebuf[EB];
+    uint2 ebuf[Geo<D>::EB];
 };
 
 // ---------------------------------------------------------------------------------------
@@ -280,13 +289,14 @@ __device__ __forceinline__ void warp_flush(const SampleArgs& a, uint2* buf, unsi
 }
 
 // append this lane's edge (if any); `fill` is warp-uniform
+template <int CAP>
 __device__ __forceinline__ void warp_emit(const SampleArgs& a, uint2* buf, unsigned& fill, bool edge, uint32_t u,
                                           uint32_t v)
 {
     const unsigned em = __ballot_sync(FULL, edge);
     if (!em) return;
     const unsigned cnt = __popc(em);
-    if (fill + cnt > (unsigned)EB) warp_flush(a, buf, fill);
+    if (fill + cnt > (unsigned)CAP) warp_flush(a, buf, fill);
     if (edge) buf[fill + __popc(em & ((1u << lane_id()) - 1u))] = make_uint2(min(u, v), max(u, v));
     fill += cnt;
 }
@@ -1275,7 +1285,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 ub = __ldg(&a.sid[ppb]);
             }
         }
-        warp_emit(a, W.ebuf, fill, edge, ua, ub);
+        warp_emit<Geo<D>::EB>(a, W.ebuf, fill, edge, ua, ub);
         // ---- (4) job setup when the dispatch slot is exhausted, then dispatch ----
         if (dnext >= dhi && more) {
             const unsigned occupied = __reduce_or_sync(FULL, chain ? (1u << ls) : 0u);
