@@ -68,7 +68,7 @@ constexpr unsigned FULL = 0xffffffffu;
 //   GIRG_G1      d = 1 task height: a job covers the 2^G1 level-l cells below one task cell
 //   GIRG_NSLOT1  d = 1 job slots per warp;  GIRG_MINB1  d = 1 resident blocks per SM
 //   GIRG_WPB3    d = 3 warps per block;     GIRG_NSLOT3 / GIRG_MINB3  d = 3 slots / blocks per SM
-//   GIRG_EB / GIRG_EB3  staged edges per warp (d != 3 / d = 3);  GIRG_MINB2  d = 2 blocks per SM
+//   GIRG_EB / GIRG_EB3  staged edges per warp (d != 3 / d = 3);  GIRG_MINB2 / GIRG_NSLOT2  d = 2 blocks per SM / job slots
 //   (d = 3: 5 blocks of 4 warps need <= 96 registers AND <= 45 KB of shared memory per block,
 //    hence the 64-entry staging buffer: 164 vs 176 ms on C5; 5 blocks without it stay at 4
 //    resident blocks with the 96-register cap and run slower, 186 ms)
@@ -91,6 +91,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef GIRG_MINB2
 #define GIRG_MINB2 4
 #endif
+#ifndef GIRG_NSLOT2
+#define GIRG_NSLOT2 4
+#endif
 #ifndef GIRG_MINB3
 #define GIRG_MINB3 5
 #endif
@@ -104,7 +107,7 @@ struct Geo {
     static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? GIRG_WPB3 : 2);  // warps per block
     static constexpr int MINB = D == 1 ? GIRG_MINB1 : (D == 2 ? GIRG_MINB2 : (D == 3 ? GIRG_MINB3 : 1));  // resident blocks per SM
     static constexpr int EB = D == 3 ? GIRG_EB3 : GIRG_EB;  // staged edges per warp (d = 3: small, so 5 blocks fit)
-    static constexpr int NSLOT = D == 1 ? GIRG_NSLOT1 : (D == 2 ? 3 : (D == 3 ? GIRG_NSLOT3 : 2));  // job slots per warp
+    static constexpr int NSLOT = D == 1 ? GIRG_NSLOT1 : (D == 2 ? GIRG_NSLOT2 : (D == 3 ? GIRG_NSLOT3 : 2));  // job slots per warp
     static constexpr int RECW = D == 1 ? 2 : (D <= 3 ? 4 : 6);       // doubles per point record
 };
 
