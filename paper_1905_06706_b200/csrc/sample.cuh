@@ -68,6 +68,8 @@ constexpr unsigned FULL = 0xffffffffu;
 //   GIRG_G1      d = 1 task height: a job covers the 2^G1 level-l cells below one task cell
 //   GIRG_NSLOT1  d = 1 job slots per warp;  GIRG_MINB1  d = 1 resident blocks per SM
 //   GIRG_WPB3    d = 3 warps per block;     GIRG_NSLOT3 / GIRG_MINB3  d = 3 slots / blocks per SM
+//   GIRG_CB3     d = 3 children per job (8 = all; 4 halves the slot but doubles the job setups:
+//                C5 214 ms at 5 blocks, 240 ms at 6 blocks / 80 registers, vs 164 ms)
 //   GIRG_EB / GIRG_EB3  staged edges per warp (d != 3 / d = 3);  GIRG_MINB2 / GIRG_NSLOT2  d = 2 blocks per SM / job slots
 //   (d = 3: 5 blocks of 4 warps need <= 96 registers AND <= 45 KB of shared memory per block,
 //    hence the 64-entry staging buffer: 164 vs 176 ms on C5; 5 blocks without it stay at 4
@@ -94,6 +96,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef GIRG_NSLOT2
 #define GIRG_NSLOT2 4
 #endif
+#ifndef GIRG_CB3
+#define GIRG_CB3 8
+#endif
 #ifndef GIRG_MINB3
 #define GIRG_MINB3 5
 #endif
@@ -103,7 +108,7 @@ struct Geo {
     static constexpr int NCH = 1 << (D * G);                 // children (= sub-cells per region parent)
     static constexpr int NPAR = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : 243;  // 3^d
     static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // lg = 1: all 2^d level-1 cells
-    static constexpr int CB = D <= 3 ? NCH : (D == 4 ? 4 : 2);        // children per job (batch)
+    static constexpr int CB = D <= 2 ? NCH : (D == 3 ? GIRG_CB3 : (D == 4 ? 4 : 2));  // children per job (batch)
     static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? GIRG_WPB3 : 2);  // warps per block
     static constexpr int MINB = D == 1 ? GIRG_MINB1 : (D == 2 ? GIRG_MINB2 : (D == 3 ? GIRG_MINB3 : 1));  // resident blocks per SM
     static constexpr int EB = D == 3 ? GIRG_EB3 : GIRG_EB;  // staged edges per warp (d = 3: small, so 5 blocks fit)
