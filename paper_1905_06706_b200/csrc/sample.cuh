@@ -68,6 +68,9 @@ constexpr unsigned FULL = 0xffffffffu;
 //   GIRG_G1      d = 1 task height: a job covers the 2^G1 level-l cells below one task cell
 //   GIRG_NSLOT1  d = 1 job slots per warp;  GIRG_MINB1  d = 1 resident blocks per SM
 //   GIRG_WPB3    d = 3 warps per block;     GIRG_NSLOT3 / GIRG_MINB3  d = 3 slots / blocks per SM
+//   GIRG_WPB1    d = 1 warps per block (d = 1 runs 5 blocks x 4 warps with 2 job slots: 96
+//                registers, 9.4 KB shared memory per warp; 2 x 8 warps with 3 slots: C4 23.5 ms
+//                vs 22.1 ms; 24 warps at 80 registers: slower)
 //   GIRG_CB3     d = 3 children per job (8 = all; 4 halves the slot but doubles the job setups:
 //                C5 214 ms at 5 blocks, 240 ms at 6 blocks / 80 registers, vs 164 ms)
 //   GIRG_EB / GIRG_EB3  staged edges per warp (d != 3 / d = 3);  GIRG_MINB2 / GIRG_NSLOT2  d = 2 blocks per SM / job slots
@@ -79,13 +82,13 @@ constexpr unsigned FULL = 0xffffffffu;
 #define GIRG_G1 4
 #endif
 #ifndef GIRG_NSLOT1
-#define GIRG_NSLOT1 3
+#define GIRG_NSLOT1 2
 #endif
 #ifndef GIRG_WPB3
 #define GIRG_WPB3 4
 #endif
 #ifndef GIRG_MINB1
-#define GIRG_MINB1 2
+#define GIRG_MINB1 5
 #endif
 #ifndef GIRG_NSLOT3
 #define GIRG_NSLOT3 2
@@ -95,6 +98,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 #ifndef GIRG_NSLOT2
 #define GIRG_NSLOT2 4
+#endif
+#ifndef GIRG_WPB1
+#define GIRG_WPB1 4
 #endif
 #ifndef GIRG_CB3
 #define GIRG_CB3 8
@@ -109,7 +115,7 @@ struct Geo {
     static constexpr int NPAR = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : 243;  // 3^d
     static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // lg = 1: all 2^d level-1 cells
     static constexpr int CB = D <= 2 ? NCH : (D == 3 ? GIRG_CB3 : (D == 4 ? 4 : 2));  // children per job (batch)
-    static constexpr int WPB = D <= 2 ? 8 : (D == 3 ? GIRG_WPB3 : 2);  // warps per block
+    static constexpr int WPB = D == 1 ? GIRG_WPB1 : (D == 2 ? 8 : (D == 3 ? GIRG_WPB3 : 2));  // warps per block
     static constexpr int MINB = D == 1 ? GIRG_MINB1 : (D == 2 ? GIRG_MINB2 : (D == 3 ? GIRG_MINB3 : 1));  // resident blocks per SM
     static constexpr int EB = D == 3 ? GIRG_EB3 : GIRG_EB;  // staged edges per warp (d = 3: small, so 5 blocks fit)
     static constexpr int NSLOT = D == 1 ? GIRG_NSLOT1 : (D == 2 ? GIRG_NSLOT2 : (D == 3 ? GIRG_NSLOT3 : 2));  // job slots per warp
