@@ -654,7 +654,7 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
     // first point of its cell; it stays first on every finer level) is <= lg.  Type-I if
     // l == CL(i,j), type-II if 2 <= l (T > 0).
     hp.tasks.clear();
-    const int G = d == 1 ? GIRG_G1 : 1;  // Geo<D>::G
+    const int G = d == 1 ? GIRG_G1 : (d == 2 ? GIRG_G2 : 1);  // Geo<D>::G
     for (int i = 0; i < p.L; ++i)
         for (int lf = 0; lf <= 32; ++lf) {
             p.toff[i * 33 + lf] = (uint32_t)hp.tasks.size();

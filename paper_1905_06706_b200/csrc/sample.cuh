@@ -66,6 +66,8 @@ constexpr unsigned FULL = 0xffffffffu;
 // Tuning knobs (compile-time; the defaults are the B200 sweep optima recorded in
 // profiles/r01/SUMMARY.md; tools/sweep_*.sh rebuild variants with -D to re-tune):
 //   GIRG_G1      d = 1 task height: a job covers the 2^G1 level-l cells below one task cell
+//   GIRG_G2      d = 2 task height (2 is parity-green but leaves the separable classification
+//                and doubles the slot: C3 9.8 -> 22-34 ms; kept at 1)
 //   GIRG_NSLOT1  d = 1 job slots per warp;  GIRG_MINB1  d = 1 resident blocks per SM
 //   GIRG_WPB3    d = 3 warps per block;     GIRG_NSLOT3 / GIRG_MINB3  d = 3 slots / blocks per SM
 //   GIRG_WPB1    d = 1 warps per block (d = 1 runs 5 blocks x 4 warps with 2 job slots: 96
@@ -78,6 +80,9 @@ constexpr unsigned FULL = 0xffffffffu;
 //    hence the 64-entry staging buffer: 164 vs 176 ms on C5; 5 blocks without it stay at 4
 //    resident blocks with the 96-register cap and run slower, 186 ms)
 // GIRG_PROFILE adds per-warp cycle / job / iteration counters (GIRG_WARP_PROFILE dumps them).
+#ifndef GIRG_G2
+#define GIRG_G2 1
+#endif
 #ifndef GIRG_G1
 #define GIRG_G1 4
 #endif
@@ -110,7 +115,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #endif
 template <int D>
 struct Geo {
-    static constexpr int G = D == 1 ? GIRG_G1 : 1;          // levels between a task cell and its children
+    static constexpr int G = D == 1 ? GIRG_G1 : (D == 2 ? GIRG_G2 : 1);  // levels between a task cell and its children
     static constexpr int NCH = 1 << (D * G);                 // children (= sub-cells per region parent)
     static constexpr int NPAR = D == 1 ? 3 : D == 2 ? 9 : D == 3 ? 27 : D == 4 ? 81 : 243;  // 3^d
     static constexpr int MAXPAR = NPAR > (1 << D) ? NPAR : (1 << D);  // lg = 1: all 2^d level-1 cells
