@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(1024) k_scan_top(uint32_t* __restrict__ bsum, 
     }
 }
 
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const uint32_t* __restrict__ in, uint64_t len,
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(uint32_t* __restrict__ in, uint64_t len,
                                                              const uint32_t* __restrict__ bsum,
                                                              uint32_t* __restrict__ out)
 {
@@ -304,7 +304,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const uint32_t* __r
 #pragma unroll
     for (int k = 0; k < SCAN_PER_THREAD; ++k) {
         const uint64_t i = base + k;
-        if (i < len) out[i] = ex;
+        if (i < len) {
+            out[i] = ex;
+            in[i] = ex + vals[k];  // the counts become scatter cursors: the cell's exclusive end
+        }
         ex += vals[k];
     }
 }
@@ -315,32 +318,32 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_final(const uint32_t* __r
 // ======================================================================================
 // K3/K4: counting-sort placement; in-cell order by vertex id (R11) and payload gather
 // ======================================================================================
-__global__ void k_scatter(const uint32_t* __restrict__ key, uint32_t n, const uint32_t* __restrict__ P,
-                          uint32_t* __restrict__ cnt, uint32_t* __restrict__ tmp, uint32_t* __restrict__ tkey)
+__global__ void k_scatter(const uint32_t* __restrict__ key, uint32_t n, uint32_t* __restrict__ cnt,
+                          uint2* __restrict__ tk)
 {
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     const uint32_t k = key[v];
-    const uint32_t slot = P[k] + atomicSub(&cnt[k], 1u) - 1u;
-    tmp[slot] = v;
-    tkey[slot] = k;
+    const uint32_t slot = atomicSub(&cnt[k], 1u) - 1u;  // cursor = P[k] + remaining count
+    tk[slot] = make_uint2(v, k);  // (id, key) in one 8-byte store: one random write per point
 }
 
 // in-cell order by vertex id (R11): the slot order of k_scatter is arbitrary inside a cell, the
 // rank of v among its cell's ids is its final position.  Writes the sorted id / key arrays and
 // the inverse permutation used by k_place.
-__global__ void k_order(const uint32_t* __restrict__ tmp, const uint32_t* __restrict__ tkey, uint32_t n,
+__global__ void k_order(const uint2* __restrict__ tk, uint32_t n,
                         const uint32_t* __restrict__ P, uint32_t* __restrict__ sid, uint32_t* __restrict__ skey,
                         uint32_t* __restrict__ inv)
 {
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const uint32_t v = tmp[s], k = tkey[s];
+    const uint2 e = tk[s];
+    const uint32_t v = e.x, k = e.y;
     const uint32_t lo = P[k], hi = P[k + 1];
     uint32_t pos = s;
     if (hi - lo > 1) {
         uint32_t rank = 0;
-        for (uint32_t t = lo; t < hi; ++t) rank += tmp[t] < v;
+        for (uint32_t t = lo; t < hi; ++t) rank += tk[t].x < v;
         pos = lo + rank;
     }
     sid[pos] = v;
@@ -708,7 +711,7 @@ static void run_wstats(const double* w, uint64_t n, cudaStream_t st, Scratch& S,
 
 template <int D>
 static void launch_index(const double* w, const double* x, uint32_t n, const Plan* d_plan, uint64_t K,
-                         uint32_t* key, uint32_t* cnt, uint32_t* P, uint32_t* bsum, uint32_t* tmp, uint32_t* tkey,
+                         uint32_t* key, uint32_t* cnt, uint32_t* P, uint32_t* bsum, uint2* tk,
                          uint32_t* inv, uint32_t* sid, uint32_t* skey, double* rec, int* d_err, cudaStream_t st)
 {
     const uint64_t len = K + 1;
@@ -718,8 +721,8 @@ static void launch_index(const double* w, const double* x, uint32_t n, const Pla
     k_scan_reduce<<<nb, SCAN_THREADS, 0, st>>>(cnt, len, bsum);
     k_scan_top<<<1, 1024, 0, st>>>(bsum, nb);
     k_scan_final<<<nb, SCAN_THREADS, 0, st>>>(cnt, len, bsum, P);
-    k_scatter<<<grid_for(n, 256), 256, 0, st>>>(key, n, P, cnt, tmp, tkey);
-    k_order<<<grid_for(n, 256), 256, 0, st>>>(tmp, tkey, n, P, sid, skey, inv);
+    k_scatter<<<grid_for(n, 256), 256, 0, st>>>(key, n, cnt, tk);
+    k_order<<<grid_for(n, 256), 256, 0, st>>>(tk, n, P, sid, skey, inv);
     k_place<D><<<grid_for(n, 256), 256, 0, st>>>(inv, n, w, x, rec);
     GCHECK(cudaGetLastError());
 }
@@ -923,8 +926,7 @@ struct EdgeCall {
         misc = S.alloc<char>(256);
         int* d_err = (int*)misc;
         uint32_t* key = S.alloc<uint32_t>(n);
-        uint32_t* tmp = S.alloc<uint32_t>(n);
-        uint32_t* tkey = S.alloc<uint32_t>(n);
+        uint2* tk = S.alloc<uint2>(n);  // (id, key) pairs in slot order
         uint32_t* inv = S.alloc<uint32_t>(n);
         uint32_t* cnt = S.alloc<uint32_t>(K + 1);
         uint32_t* P = S.alloc<uint32_t>(K + 1);
@@ -952,11 +954,11 @@ struct EdgeCall {
         GCHECK(cudaMemsetAsync(misc, 0, 256, st));
         PE.record(1, st);
         switch (d) {
-            case 1: launch_index<1>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
-            case 2: launch_index<2>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
-            case 3: launch_index<3>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
-            case 4: launch_index<4>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
-            default: launch_index<5>(w, x, n32, d_plan, K, key, cnt, P, bsum, tmp, tkey, inv, sid, skey, rec, d_err, st); break;
+            case 1: launch_index<1>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, d_err, st); break;
+            case 2: launch_index<2>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, d_err, st); break;
+            case 3: launch_index<3>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, d_err, st); break;
+            case 4: launch_index<4>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, d_err, st); break;
+            default: launch_index<5>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, d_err, st); break;
         }
         a.pl = d_plan;
         a.tab = d_tab;
