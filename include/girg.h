@@ -52,6 +52,8 @@ typedef struct {
     uint64_t key_space;  /* number of index cells sum_i 2^(d I(i))               */
     uint64_t fast_fallback; /* decisions the float fast path left to the canonical double path */
     uint64_t fast_mismatch; /* fast-path decisions that differ from the canonical one (must be 0) */
+    uint64_t neartie_jump;  /* jump quotient z within 1e-15 max(1,|z|) of an integer where it can
+                               matter (z < remaining + 1), R21 (device-side)          */
 } girg_stats;
 
 /*

@@ -40,7 +40,7 @@ class Stats(C.Structure):
     _fields_ = [(name, C.c_uint64) for name in (
         "visits", "ev1", "ev1_nonempty", "cand1", "acc1",
         "ev2", "ev2_nonempty", "chunks", "draws", "landings", "acc2",
-        "nt1", "nt2acc", "nt2jump", "cand2", "ns_pre", "ns_edges")]
+        "nt1", "nt2acc", "nt2jump", "cand2", "ns_pre", "ns_edges", "rnd1", "jchk")]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}
@@ -95,6 +95,7 @@ def lib():
         L.or_coverage.argtypes = [dp, dp, u64, i32, d, d, i32, u32p, C.POINTER(Stats)]; L.or_coverage.restype = i32
         L.or_index.argtypes = [dp, dp, u64, i32, d, u32p, u64p, u32p, u64p, u64]; L.or_index.restype = i32
         L.or_count_pairs.argtypes = [i32, i32, u64p, u64p, u64p, u64p]; L.or_count_pairs.restype = i32
+        L.or_set_tie_hook.argtypes = [i32, d]
     return _lib
 
 
@@ -283,6 +284,11 @@ def scale_weights(w, avg_deg, d, T, beta) -> float:
 
 def geometric_skip(p, u) -> int:
     return int(lib().or_geometric_skip(p, u))
+
+
+def set_tie_hook(mode: int, delta: float = 0.0):
+    """TEST HOOK (O12 pin): perturb decision variables to threshold + delta (0 = off)."""
+    lib().or_set_tie_hook(int(mode), float(delta))
 
 
 def sort_edges(e: np.ndarray) -> np.ndarray:

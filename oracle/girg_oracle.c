@@ -53,6 +53,21 @@ double or_u53(uint32_t hi, uint32_t lo)
     return (double)b * 0x1p-53;
 }
 
+/* TEST HOOK for the near-tie detector (O12 pin, tests/test_oracle_sampler.py): when a mode
+ * bit is set, the decision variable of that kind is moved to (threshold + delta) before the
+ * detector and the decision run, so a test can check that the detector fires inside its window
+ * and stays silent outside it, on every decision of that kind.  Bit 1: type-I uniform
+ * r := p_uv + delta (decisions with p_uv < 1).  Bit 2: type-II acceptance r_acc := p_uv/pbar +
+ * delta.  Bit 4: jump quotient z := nearbyint(z) + delta*max(1,|z|).  Off (0) by default; never
+ * set outside tests. */
+static int or_tie_mode = 0;
+static double or_tie_delta = 0.0;
+void or_set_tie_hook(int mode, double delta)
+{
+    or_tie_mode = mode;
+    or_tie_delta = delta;
+}
+
 /* ===================================================================================== */
 /* Model, Sec. 2.1                                                           */
 /* ===================================================================================== */
@@ -405,6 +420,8 @@ static void type1(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
                     uint32_t ctr[4] = {u < v ? u : v, u < v ? v : u, 0u, 3u}, o[4];
                     or_philox4x32_10(ctr, c->seed, o);
                     double r = or_u53(o[0], o[1]);
+                    if (or_tie_mode & 1) r = p + or_tie_delta;
+                    c->st->rnd1++;
                     if (fabs(r - p) < 1e-12) c->st->nt1++;
                     edge = r < p;
                 }
@@ -466,7 +483,12 @@ static void type2(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
              * log are each within 1 ulp of log(1-rj), the division is correctly rounded, so the
              * two z differ by < 3 ulp < 7e-16 |z|; only a z within 1e-15 |z| of an integer, and
              * small enough to matter (z < remaining + 1), is counted. */
+            if ((or_tie_mode & 4) && pbar < 1.0) {
+                double az0 = fabs(z);
+                z = nearbyint(z) + or_tie_delta * (az0 > 1.0 ? az0 : 1.0);
+            }
             if (z < (double)remaining + 1.0 && pbar < 1.0) {
+                c->st->jchk++;
                 double az = fabs(z);
                 if (fabs(z - nearbyint(z)) < 1e-15 * (az > 1.0 ? az : 1.0)) c->st->nt2jump++;
             }
@@ -478,6 +500,7 @@ static void type2(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
             double D = or_dpow(or_torus_dist(xcoord(c, u, xu), xcoord(c, v, xv), c->d), c->d);
             double p = or_prob(c->w[u], c->w[v], c->s, D, c->T);
             /* acceptance near-tie: the uniform r_acc within 1e-12 of its threshold p_uv/pbar */
+            if (or_tie_mode & 2) ra = p / pbar + or_tie_delta;
             if (fabs(ra * pbar - p) < 1e-12 * pbar) c->st->nt2acc++;
             if (ra * pbar < p) { c->st->acc2++; emit(c, u, v); }
         }
@@ -601,7 +624,12 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
             double rj = or_u53(o[0], o[1]), ra = or_u53(o[2], o[3]);
             double z = pbar == 1.0 ? 0.0 : log(1.0 - rj) / Lbar;
             int64_t remaining = (int64_t)end - pos - 1;
+            if ((or_tie_mode & 4) && pbar < 1.0) {
+                double az0 = fabs(z);
+                z = nearbyint(z) + or_tie_delta * (az0 > 1.0 ? az0 : 1.0);
+            }
             if (z < (double)remaining + 1.0 && pbar < 1.0) { /* jump near-tie, as in type2 */
+                c->st->jchk++;
                 double az = fabs(z);
                 if (fabs(z - nearbyint(z)) < 1e-15 * (az > 1.0 ? az : 1.0)) c->st->nt2jump++;
             }
@@ -614,6 +642,7 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
             uint32_t u = Va[a0 + sidx], v = Vb[b0[t] + (tidx - pre[t])];
             double D = or_dpow(or_torus_dist(xcoord(c, u, xu), xcoord(c, v, xv), c->d), c->d);
             double p = or_prob(c->w[u], c->w[v], c->s, D, c->T);
+            if (or_tie_mode & 2) ra = p / pbar + or_tie_delta;
             if (fabs(ra * pbar - p) < 1e-12 * pbar) c->st->nt2acc++;
             if (ra * pbar < p) { c->st->acc2++; emit(c, u, v); }
         }

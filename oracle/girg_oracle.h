@@ -71,7 +71,13 @@ typedef struct {
     uint64_t nt1, nt2acc, nt2jump; /* near-ties: type-I r~p, type-II r_acc~p/pbar, jump z~int */
     uint64_t cand2;                /* sum of |V_i^A||V_j^B| over type-II events */
     uint64_t ns_pre, ns_edges;     /* wall time: levels + index ("Pre"), recursion ("Edges") */
+    uint64_t rnd1;                 /* type-I decisions that drew a uniform (p_uv < 1) */
+    uint64_t jchk;                 /* jump near-tie checks (draws with z < remaining + 1) */
 } or_stats_t;
+
+/* TEST HOOK (O12 pin): move type-I uniforms (bit 1), type-II acceptance uniforms (bit 2) or
+ * jump quotients (bit 4) to threshold + delta; 0 = off (the default) */
+void or_set_tie_hook(int mode, double delta);
 
 /* type-II schemes: EVENT = one jump sequence per distant cell pair (Alg. 1 lines 5-6 as
  * written, R10); MERGED = one sequence per (A cell, bound class), the distant pairs of A with

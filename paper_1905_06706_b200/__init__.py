@@ -35,7 +35,7 @@ _lib = C.CDLL(_LIB_PATH)
 class Stats(C.Structure):
     _fields_ = [(k, C.c_uint64) for k in (
         "cand1", "ev2", "chunks", "draws", "landings", "edges1", "edges2",
-        "neartie1", "neartie2", "layers", "key_space", "fast_fallback", "fast_mismatch")]
+        "neartie1", "neartie2", "layers", "key_space", "fast_fallback", "fast_mismatch", "neartie_jump")]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}
@@ -102,6 +102,21 @@ def _dev_f64(t: torch.Tensor, name: str) -> torch.Tensor:
     return t
 
 
+def _edge_buf(t: torch.Tensor, name: str, cuda: bool) -> int:
+    """An edge buffer must be a contiguous int32 [cap, 2] tensor (the kernels write 2*cap words)."""
+    if not (t.dtype == torch.int32 and t.dim() == 2 and t.shape[1] == 2 and t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous int32 tensor of shape [cap, 2]")
+    if t.is_cuda != cuda:
+        raise ValueError(f"{name} must be a {'CUDA' if cuda else 'host'} tensor")
+    return t.shape[0]
+
+
+def _host_f64(t: torch.Tensor, name: str, numel: int) -> torch.Tensor:
+    if not (not t.is_cuda and t.dtype == torch.float64 and t.is_contiguous() and t.numel() == numel):
+        raise ValueError(f"{name} must be a contiguous float64 host tensor with {numel} elements")
+    return t
+
+
 def library_path() -> str:
     return _LIB_PATH
 
@@ -148,10 +163,19 @@ def edges(w: torch.Tensor, x: torch.Tensor, T: float, kappa: float, seed: int, c
     d = x.numel() // n
     if x.numel() != d * n:
         raise ValueError("x must have d*n elements")
+    if x.device != w.device:
+        raise ValueError("w and x must be on the same device")
     if out is not None:
-        cap = out.shape[0]
+        cap = _edge_buf(out, "out", cuda=True)
+        if out.device != w.device:
+            raise ValueError("out must be on the device of w")
     elif cap is None:
         cap = 16 * n + 1024
+    with torch.cuda.device(w.device):
+        return _edges_on_device(w, x, n, d, T, kappa, seed, cap, out, shard, stats, stream, scheme)
+
+
+def _edges_on_device(w, x, n, d, T, kappa, seed, cap, out, shard, stats, stream, scheme):
     for _ in range(2):
         buf = out if out is not None else torch.empty((cap, 2), dtype=torch.int32, device=w.device)
         m = C.c_uint64(0)
@@ -171,9 +195,12 @@ def edges(w: torch.Tensor, x: torch.Tensor, T: float, kappa: float, seed: int, c
 def edges_host(w_host, x_host, d: int, T: float, kappa: float, seed: int, out_host, stream=None) -> int:
     """End-to-end call with HOST (ideally pinned) tensors: returns m; edges in out_host[:m]."""
     n = w_host.numel()
+    _host_f64(w_host, "w_host", n)
+    _host_f64(x_host, "x_host", d * n)
+    cap = _edge_buf(out_host, "out_host", cuda=False)
     m = C.c_uint64(0)
     _check(_lib.girg_edges_host(w_host.data_ptr(), x_host.data_ptr(), n, d, T, kappa, seed, out_host.data_ptr(),
-                                out_host.shape[0], C.byref(m), _stream(stream)))
+                                cap, C.byref(m), _stream(stream)))
     return int(m.value)
 
 

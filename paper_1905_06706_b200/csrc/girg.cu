@@ -330,10 +330,13 @@ __global__ void k_scatter(const uint32_t* __restrict__ key, uint32_t n, uint32_t
 
 // in-cell order by vertex id (R11): the slot order of k_scatter is arbitrary inside a cell, the
 // rank of v among its cell's ids is its final position.  Writes the sorted id / key arrays and
-// the inverse permutation used by k_place.
+// the inverse permutation used by k_place.  Cells of <= ORDER_SMALL points rank each point by
+// scanning the cell (<= ORDER_SMALL^2 reads per cell); larger cells are listed for k_order_big
+// (a linear-time radix sort per cell), so crowded cells cost O(c), not O(c^2).
+constexpr uint32_t ORDER_SMALL = 32;
 __global__ void k_order(const uint2* __restrict__ tk, uint32_t n,
                         const uint32_t* __restrict__ P, uint32_t* __restrict__ sid, uint32_t* __restrict__ skey,
-                        uint32_t* __restrict__ inv)
+                        uint32_t* __restrict__ inv, uint32_t* __restrict__ big, uint32_t* __restrict__ nbig)
 {
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
@@ -341,6 +344,14 @@ __global__ void k_order(const uint2* __restrict__ tk, uint32_t n,
     const uint32_t v = e.x, k = e.y;
     const uint32_t lo = P[k], hi = P[k + 1];
     uint32_t pos = s;
+    if (hi - lo > ORDER_SMALL) {
+        if (s == lo) {
+            const uint32_t q = atomicAdd(nbig, 1u);
+            big[2 * q] = lo;
+            big[2 * q + 1] = hi;
+        }
+        return;
+    }
     if (hi - lo > 1) {
         uint32_t rank = 0;
         for (uint32_t t = lo; t < hi; ++t) rank += tk[t].x < v;
@@ -349,6 +360,85 @@ __global__ void k_order(const uint2* __restrict__ tk, uint32_t n,
     sid[pos] = v;
     skey[pos] = k;
     inv[v] = pos;
+}
+
+// the cells k_order listed: one block per cell (grid-stride over the list), LSD radix sort of
+// the cell's vertex ids by 8-bit digits, each pass a stable scatter (per-warp match + per-digit
+// prefix over the block's warps), ping-ponging between sid[lo..hi) and tmp[lo..hi) (the key
+// array, free after k_scatter).  O(c) per pass per cell.
+constexpr int OB_THREADS = 256, OB_WARPS = OB_THREADS / 32;
+__global__ void __launch_bounds__(OB_THREADS) k_order_big(const uint2* __restrict__ tk, int passes,
+                                                         const uint32_t* __restrict__ big,
+                                                         const uint32_t* __restrict__ nbig,
+                                                         uint32_t* __restrict__ sid, uint32_t* __restrict__ skey,
+                                                         uint32_t* __restrict__ inv, uint32_t* __restrict__ tmp)
+{
+    __shared__ uint32_t base[256];
+    __shared__ uint32_t wcnt[OB_WARPS][256];
+    const unsigned tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+    const uint32_t nb = *nbig;
+    for (uint32_t q = blockIdx.x; q < nb; q += gridDim.x) {
+        const uint32_t lo = big[2 * q], hi = big[2 * q + 1], c = hi - lo, key = tk[lo].y;
+        for (int pass = 0; pass < passes; ++pass) {
+            const int sh = 8 * pass;
+            // source of this pass: tk ids (pass 0), then alternately sid / tmp
+            const uint32_t* src = pass == 0 ? nullptr : ((pass & 1) ? sid : tmp);
+            uint32_t* dst = (pass & 1) ? tmp : sid;
+            for (int k = tid; k < 256; k += OB_THREADS) base[k] = 0;
+            for (int k = tid; k < OB_WARPS * 256; k += OB_THREADS) (&wcnt[0][0])[k] = 0;
+            __syncthreads();
+            for (uint32_t t = tid; t < c; t += OB_THREADS) {
+                const uint32_t id = src ? src[lo + t] : tk[lo + t].x;
+                atomicAdd(&base[(id >> sh) & 255u], 1u);
+            }
+            __syncthreads();
+            if (tid == 0) {  // exclusive scan of the digit histogram (256 entries)
+                uint32_t acc = 0;
+                for (int k = 0; k < 256; ++k) {
+                    const uint32_t x = base[k];
+                    base[k] = acc;
+                    acc += x;
+                }
+            }
+            __syncthreads();
+            for (uint32_t t0 = 0; t0 < c; t0 += OB_THREADS) {
+                const uint32_t t = t0 + tid;
+                const bool ok = t < c;
+                uint32_t id = 0, dg = 0, wr = 0;
+                const unsigned act = __ballot_sync(0xffffffffu, ok);
+                if (ok) {
+                    id = src ? src[lo + t] : tk[lo + t].x;
+                    dg = (id >> sh) & 255u;
+                    const unsigned peers = __match_any_sync(act, dg);
+                    wr = __popc(peers & ((1u << lane) - 1u));
+                    if (wr == 0) wcnt[warp][dg] = __popc(peers);
+                }
+                __syncthreads();
+                for (int k = tid; k < 256; k += OB_THREADS) {  // per digit: prefix over the warps
+                    uint32_t run = base[k];
+                    for (int w2 = 0; w2 < OB_WARPS; ++w2) {
+                        const uint32_t x = wcnt[w2][k];
+                        wcnt[w2][k] = run;
+                        run += x;
+                    }
+                    base[k] = run;
+                }
+                __syncthreads();
+                if (ok) dst[lo + wcnt[warp][dg] + wr] = id;
+                __syncthreads();
+                for (int k = tid; k < OB_WARPS * 256; k += OB_THREADS) (&wcnt[0][0])[k] = 0;
+                __syncthreads();
+            }
+        }
+        const uint32_t* fin = (passes & 1) ? sid : tmp;
+        for (uint32_t t = tid; t < c; t += OB_THREADS) {
+            const uint32_t v = fin[lo + t];
+            if (fin != sid) sid[lo + t] = v;
+            skey[lo + t] = key;
+            inv[v] = lo + t;
+        }
+        __syncthreads();
+    }
 }
 
 // sorted point records rec[pos] = (x_0, .., x_{d-1}, w): coalesced reads in vertex order,
@@ -709,10 +799,28 @@ static void run_wstats(const double* w, uint64_t n, cudaStream_t st, Scratch& S,
     std::memcpy(parts.data(), h.data() + HIST_BINS * sizeof(uint32_t) + 16, nb * sizeof(WPartial));
 }
 
+// SM count of the current device (queried once per device)
+static int device_sms()
+{
+    static std::mutex mu;
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
 template <int D>
 static void launch_index(const double* w, const double* x, uint32_t n, const Plan* d_plan, uint64_t K,
                          uint32_t* key, uint32_t* cnt, uint32_t* P, uint32_t* bsum, uint2* tk,
-                         uint32_t* inv, uint32_t* sid, uint32_t* skey, double* rec, int* d_err, cudaStream_t st)
+                         uint32_t* inv, uint32_t* sid, uint32_t* skey, double* rec, uint32_t* big, uint32_t* nbig,
+                         int* d_err, cudaStream_t st)
 {
     const uint64_t len = K + 1;
     GCHECK(cudaMemsetAsync(cnt, 0, len * sizeof(uint32_t), st));
@@ -722,21 +830,31 @@ static void launch_index(const double* w, const double* x, uint32_t n, const Pla
     k_scan_top<<<1, 1024, 0, st>>>(bsum, nb);
     k_scan_final<<<nb, SCAN_THREADS, 0, st>>>(cnt, len, bsum, P);
     k_scatter<<<grid_for(n, 256), 256, 0, st>>>(key, n, cnt, tk);
-    k_order<<<grid_for(n, 256), 256, 0, st>>>(tk, n, P, sid, skey, inv);
+    k_order<<<grid_for(n, 256), 256, 0, st>>>(tk, n, P, sid, skey, inv, big, nbig);
+    {
+        int bits = 1;
+        while (bits < 32 && (1ull << bits) < (unsigned long long)n) ++bits;
+        const unsigned gb = (unsigned)std::min<uint64_t>((uint64_t)device_sms() * 4u, n / (ORDER_SMALL + 1) + 1);
+        k_order_big<<<gb, OB_THREADS, 0, st>>>(tk, (bits + 7) / 8, big, nbig, sid, skey, inv, key);
+    }
     k_place<D><<<grid_for(n, 256), 256, 0, st>>>(inv, n, w, x, rec);
     GCHECK(cudaGetLastError());
 }
 
+// dynamic shared memory opt-in; the attribute is per device, so the cache is keyed by
+// (device, kernel)
 template <class K>
 static void smem_optin(K kern, size_t bytes)
 {
-    static thread_local std::vector<const void*> done;
+    static thread_local std::vector<std::pair<int, const void*>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
     const void* f = (const void*)kern;
-    for (const void* q : done)
-        if (q == f) return;
+    for (const auto& q : done)
+        if (q.first == dev && q.second == f) return;
     GCHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     GCHECK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    done.push_back(f);
+    done.emplace_back(dev, f);
 }
 
 template <int D, int SCHEME, bool STATS>
@@ -747,12 +865,7 @@ static void launch_sample_t(const SampleArgs& a, cudaStream_t st)
     smem_optin(k_sample<D, SCHEME, STATS>, smem);
     smem_optin(k_big<D, SCHEME, STATS>, smem);
     // SM count and occupancies queried once per instantiation (one GPU type per process)
-    static const int nsm = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
+    const int nsm = device_sms();
     static const int occ = [] {
         int v = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_sample<D, SCHEME, STATS>, TPB, sizeof(WarpSmem<D>) * WPB);
@@ -918,7 +1031,8 @@ struct EdgeCall {
                      up_bytes = up_plan + up_tab + hp.tasks.size() * sizeof(uint16_t);
         S.reserve(Scratch::rounded(up_bytes) + Scratch::rounded(256) + 6 * Scratch::rounded(n * 4) +
                   2 * Scratch::rounded((K + 1) * 4) + Scratch::rounded((grid_for(K + 1, SCAN_TILE) + 1) * 4) +
-                  Scratch::rounded((size_t)recw * n * 8) + Scratch::rounded((size_t)items_cap * sizeof(BigItem)));
+                  Scratch::rounded((size_t)recw * n * 8) + Scratch::rounded((size_t)items_cap * sizeof(BigItem)) +
+                  Scratch::rounded((2 * (n / (ORDER_SMALL + 1) + 1)) * 4));
         char* d_up = S.alloc<char>(up_bytes);
         Plan* d_plan = (Plan*)d_up;
         TabEntry* d_tab = (TabEntry*)(d_up + up_plan);
@@ -935,6 +1049,8 @@ struct EdgeCall {
         uint32_t* skey = S.alloc<uint32_t>(n);
         double* rec = S.alloc<double>((size_t)recw * n);
         BigItem* items = S.alloc<BigItem>(items_cap);
+        uint32_t* big = S.alloc<uint32_t>(2 * (n / (ORDER_SMALL + 1) + 1));  // crowded cells for k_order_big
+        uint32_t* nbig = (uint32_t*)(misc + 132);
         // plan, bound table and task lists in one upload from page-locked staging (the weight
         // statistics above are consumed); the staging tail receives the status block
         char* stage = PE.staging(up_bytes + 256);
@@ -954,11 +1070,11 @@ struct EdgeCall {
         GCHECK(cudaMemsetAsync(misc, 0, 256, st));
         PE.record(1, st);
         switch (d) {
-            case 1: launch_index<1>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, d_err, st); break;
-            case 2: launch_index<2>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, d_err, st); break;
-            case 3: launch_index<3>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, d_err, st); break;
-            case 4: launch_index<4>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, d_err, st); break;
-            default: launch_index<5>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, d_err, st); break;
+            case 1: launch_index<1>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, big, nbig, d_err, st); break;
+            case 2: launch_index<2>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, big, nbig, d_err, st); break;
+            case 3: launch_index<3>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, big, nbig, d_err, st); break;
+            case 4: launch_index<4>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, big, nbig, d_err, st); break;
+            default: launch_index<5>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, big, nbig, d_err, st); break;
         }
         a.pl = d_plan;
         a.tab = d_tab;
@@ -1035,7 +1151,7 @@ struct EdgeCall {
         g_timings.ms_index = PE.ms(1, 2);
         g_timings.ms_sample = PE.ms(2, 3);
         g_timings.ms_total = PE.ms(0, 3);
-        g_timings.launches = 10;  // k_wstats, k_keys, 3 x scan, k_scatter, k_order, k_place, k_sample, k_big
+        g_timings.launches = 11;  // k_wstats, k_keys, 3 x scan, k_scatter, k_order, k_order_big, k_place, k_sample, k_big
         g_timings.n = n;
         g_timings.key_space = hp.K;
         g_timings.d = d;
@@ -1061,6 +1177,7 @@ struct EdgeCall {
             stats_out->neartie2 = hc.nt2;
             stats_out->fast_fallback = hc.fb;
             stats_out->fast_mismatch = hc.mm;
+            stats_out->neartie_jump = hc.ntj;
             stats_out->layers = (uint64_t)hp.p.L;
             stats_out->key_space = hp.K;
         }
@@ -1084,8 +1201,11 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         return E.stage_c();
     } catch (const CudaFail& f) {
         return map_cuda(f.e);
-    } catch (...) {
+    } catch (const std::bad_alloc&) {
         return GIRG_ENOMEM;
+    } catch (...) {
+        g_last_cuda = "internal error: unexpected exception";
+        return GIRG_ECUDA;
     }
 }
 
@@ -1217,7 +1337,7 @@ static void estimator_tail(const double* w, uint64_t n, Estimator& E, cudaStream
     uint32_t cap = 1u << 16;
     for (;;) {
         Scratch S(st);
-        const unsigned nb = std::min<unsigned>(grid_for(n, SUM_THREADS), 148u * 8u);
+        const unsigned nb = std::min<unsigned>(grid_for(n, SUM_THREADS), (unsigned)device_sms() * 8u);
         TailSums* d_part = S.alloc<TailSums>(nb);
         double* d_cand = S.alloc<double>(cap);
         uint32_t* d_nc = S.alloc<uint32_t>(1);
@@ -1326,8 +1446,11 @@ static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double
         return GIRG_OK;
     } catch (const CudaFail& fl) {
         return map_cuda(fl.e);
-    } catch (...) {
+    } catch (const std::bad_alloc&) {
         return GIRG_ENOMEM;
+    } catch (...) {
+        g_last_cuda = "internal error: unexpected exception";
+        return GIRG_ECUDA;
     }
 }
 
@@ -1421,8 +1544,11 @@ extern "C" int girg_edges_host(const double* w_host, const double* x_host, uint6
         return GIRG_OK;
     } catch (const CudaFail& f) {
         return map_cuda(f.e);
-    } catch (...) {
+    } catch (const std::bad_alloc&) {
         return GIRG_ENOMEM;
+    } catch (...) {
+        g_last_cuda = "internal error: unexpected exception";
+        return GIRG_ECUDA;
     }
 }
 

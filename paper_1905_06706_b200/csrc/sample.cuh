@@ -145,7 +145,7 @@ struct MaskOf<16> {
 };
 
 struct Counters {
-    unsigned long long cand1, ev2, chunks, draws, landings, edges1, edges2, nt1, nt2, fb, mm;
+    unsigned long long cand1, ev2, chunks, draws, landings, edges1, edges2, nt1, nt2, fb, mm, ntj;
 };
 
 // one (child, kind) sequence of a job (its unit count is the difference of the slot's uoff)
@@ -980,6 +980,7 @@ __device__ __forceinline__ void flush_counters(const SampleArgs& a, const Counte
     atomicAdd(&a.stats->nt2, c.nt2);
     atomicAdd(&a.stats->fb, c.fb);
     atomicAdd(&a.stats->mm, c.mm);
+    atomicAdd(&a.stats->ntj, c.ntj);
 }
 
 // queue a job's unit range as items of ~ITEM_WORK weighted units (lane 0)
@@ -1241,6 +1242,9 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 if (STATS) {
                     if (st < 0) ++C.fb;
                     else C.mm += (st != st2) || (st == 0 && skip != (long long)z);
+                    // jump near-tie (R21), the oracle's O12 rule evaluated on the device's own z
+                    if (pb_ < 1.0 && z < (double)remaining + 1.0 && fabs(z - rint(z)) < 1e-15 * fmax(1.0, fabs(z)))
+                        ++C.ntj;
                 }
                 st = st2;
                 skip = st2 ? 0 : (long long)z;

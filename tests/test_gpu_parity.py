@@ -3,8 +3,10 @@
 Inputs come from workloads.synth_inputs (numpy PCG64, shared by both sides) or from each side's
 own generator (H1/H2 parity).  kappa always comes from the oracle's estimator, never from the
 CUDA path.  T = 0: bit-exact edge sets.  T > 0: identical edge sets, with the oracle's near-tie
-counters (|r - p| < 1e-12, |r_acc - p/pbar| < 1e-12, jump z within 1e-14|z| of an integer)
-required to be zero.
+counters (|r - p| < 1e-12, |r_acc - p/pbar| < 1e-12, jump z within 1e-15 max(1,|z|) of an
+integer, R14/R21) required to be zero, and the device's own counters of the same
+near-ties and of fast-path disagreements too.  Every parity case runs both the production
+kernels (stats=False) and the counting build (stats=True).
 """
 import numpy as np
 import pytest
@@ -30,16 +32,29 @@ def gpu_keys(e):
 
 
 def run_both(w, x, d, T, kappa, seed, shard=(0, 0, 1), scheme=girg.SCHEME_MERGED):
-    e, st = girg.edges(dev(w), dev(x), T, kappa, seed, shard=shard, stats=True, scheme=scheme)
+    """The production kernels (stats=False: the float fast paths decide) and the counting build
+    (stats=True: every decision also taken canonically, disagreements counted) against the
+    oracle on the same inputs."""
+    wd, xd = dev(w), dev(x)
+    e, st = girg.edges(wd, xd, T, kappa, seed, shard=shard, stats=True, scheme=scheme)
+    ep = girg.edges(wd, xd, T, kappa, seed, shard=shard, stats=False, scheme=scheme)
     eo, so = O.edges(w, x, d, T, kappa, seed, shard=shard, with_stats=True, scheme=scheme)
-    return gpu_keys(e), O.sort_edges(eo), st, so
+    return gpu_keys(e), O.sort_edges(eo), st, so, gpu_keys(ep)
+
+
+def assert_device_clean(st):
+    """Device-side near-tie counters (type-I, acceptance, jump) and fast-path disagreements."""
+    assert st["neartie1"] == 0 and st["neartie2"] == 0 and st["neartie_jump"] == 0, st
+    assert st["fast_mismatch"] == 0, st
 
 
 def assert_parity(w, x, d, T, kappa, seed, shard=(0, 0, 1), scheme=girg.SCHEME_MERGED):
-    g, o, st, so = run_both(w, x, d, T, kappa, seed, shard, scheme)
+    g, o, st, so, gp = run_both(w, x, d, T, kappa, seed, shard, scheme)
     assert so["nt1"] + so["nt2acc"] + so["nt2jump"] == 0, so
     assert len(g) == len(o), (len(g), len(o))
     assert np.array_equal(g, o)
+    assert np.array_equal(gp, o)  # the production (stats=False) kernels too
+    assert_device_clean(st)
     # the device's own work counters agree with the oracle's
     assert st["cand1"] == so["cand1"]
     assert st["landings"] == so["landings"] and st["draws"] == so["draws"]
@@ -138,16 +153,16 @@ def test_C5_sampled_shard_parity():
     full, st = girg.edges(wd, xd, c.T, kappa, c.seed, stats=True)
     m = full.shape[0]
     assert abs(2 * m / c.n - c.avg_deg) < 0.01 * c.avg_deg
-    assert st["neartie1"] == 0 and st["neartie2"] == 0 and st["fast_mismatch"] == 0
+    assert_device_clean(st)
     k = girg.edge_keys(full)  # sorted int64 keys on the device
     assert bool((k[1:] != k[:-1]).all())  # no duplicates
     u, v = k >> 32, k & 0xFFFFFFFF
     assert bool((u < v).all()) and bool((v < c.n).all())
     total = 0
     for lo, hi in ((0, 1), (137, 138), (511, 512)):
-        g, o, stg, so = run_both(w, x, c.d, c.T, kappa, c.seed, shard=(3, lo, hi))
+        g, o, stg, so, gp = run_both(w, x, c.d, c.T, kappa, c.seed, shard=(3, lo, hi))
         assert so["nt1"] + so["nt2acc"] + so["nt2jump"] == 0, so
-        assert np.array_equal(g, o)
+        assert np.array_equal(g, o) and np.array_equal(gp, o)
         gd = torch.from_numpy(g.astype(np.int64)).cuda()
         pos = torch.searchsorted(k, gd).clamp(max=m - 1)
         assert bool((k[pos] == gd).all())  # the shard is a subset of the full graph
@@ -333,3 +348,19 @@ def test_big_job_items_and_queue_regrowth(monkeypatch):
     assert np.array_equal(gpu_keys(got), gpu_keys(ref))
     assert st1["landings"] == st0["landings"] and st1["cand1"] == st0["cand1"]
     assert st1["cand1"] + st1["chunks"] > (1 << 18)  # more 1-unit items than the initial queue
+
+
+@pytest.mark.parametrize("d,T,nc,kappa", [(1, 0.0, 30_000, 1e-9), (2, 0.6, 3_000, 1e-19)])
+def test_crowded_cell_linear_order(d, T, nc, kappa):
+    """One cell holding nc points (a tight cluster, far more than the insertion level expects):
+    k_order lists it and k_order_big radix-sorts its ids in linear time (several 256-point
+    tiles, 3 digit passes for n = 10^5); the in-cell id order (R11) and so the edge set must
+    still equal the oracle's."""
+    n, beta = 100_000, 2.5
+    w, x = synth_inputs(n, d, beta, 606)
+    rng = np.random.default_rng(5)
+    idx = rng.choice(n, nc, replace=False)
+    for k in range(d):
+        x[k, idx] = 0.5 + rng.integers(0, 1 << 20, size=idx.size) * 2.0**-53  # width 1.2e-10
+    g, st, so = assert_parity(w, x, d, T, kappa, 3)
+    assert len(g) > 1000

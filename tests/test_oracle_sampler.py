@@ -199,3 +199,44 @@ def test_T_to_zero_limit(oracle, d):
         sizes.append(diff)
     assert sizes[0] >= sizes[-1]
     assert sizes[-1] <= 3
+
+
+@SCHEMES
+def test_near_tie_detector_fires_inside_window_only(oracle, scheme):
+    """O12 pin (north-star parity rule; R14, R21): the near-tie detector must fire on
+    EVERY decision whose variable lies inside its window and on none outside it.  The test hook
+    moves each decision variable to threshold + delta: type-I r := p_uv + delta (window 1e-12),
+    type-II acceptance r_acc := p_uv/pbar + delta (window 1e-12 in r_acc), jump quotient
+    z := round(z) + delta*max(1,|z|) (window 1e-15 relative).  Without the hook the counters are
+    zero on the same graph, so "zero near-ties" in the parity runs is evidence, not a detector
+    that never fires."""
+    w, x = synth_inputs(3000, 2, 2.4, 501)
+    kappa = oracle.scale_weights(w, 10.0, 2, 0.6, 2.4)
+    try:
+        _, base = oracle.edges(w, x, 2, 0.6, kappa, 9, with_stats=True, scheme=scheme)
+        assert base["nt1"] == base["nt2acc"] == base["nt2jump"] == 0
+        assert base["rnd1"] > 100 and base["landings"] > 100 and base["jchk"] > 100
+        for delta in (0.0, 0.25e-12, -0.25e-12, 0.9e-12):  # inside the 1e-12 windows
+            oracle.set_tie_hook(1, delta)
+            _, s = oracle.edges(w, x, 2, 0.6, kappa, 9, with_stats=True, scheme=scheme)
+            assert s["nt1"] == s["rnd1"] > 0, (delta, s)
+            oracle.set_tie_hook(2, delta)
+            _, s = oracle.edges(w, x, 2, 0.6, kappa, 9, with_stats=True, scheme=scheme)
+            assert s["nt2acc"] == s["landings"] > 0, (delta, s)
+        for delta in (1.1e-12, -1.1e-12, 4e-12, 1e-9):  # outside
+            oracle.set_tie_hook(1, delta)
+            _, s = oracle.edges(w, x, 2, 0.6, kappa, 9, with_stats=True, scheme=scheme)
+            assert s["nt1"] == 0 and s["rnd1"] > 0, (delta, s)
+            oracle.set_tie_hook(2, delta)
+            _, s = oracle.edges(w, x, 2, 0.6, kappa, 9, with_stats=True, scheme=scheme)
+            assert s["nt2acc"] == 0 and s["landings"] > 0, (delta, s)
+        for delta in (0.0, 0.25e-15, -0.5e-15):  # jump: inside 1e-15 |z|
+            oracle.set_tie_hook(4, delta)
+            _, s = oracle.edges(w, x, 2, 0.6, kappa, 9, with_stats=True, scheme=scheme)
+            assert s["nt2jump"] == s["jchk"] > 0, (delta, s)
+        for delta in (2e-15, -4e-15, 1e-9):
+            oracle.set_tie_hook(4, delta)
+            _, s = oracle.edges(w, x, 2, 0.6, kappa, 9, with_stats=True, scheme=scheme)
+            assert s["nt2jump"] == 0 and s["jchk"] > 0, (delta, s)
+    finally:
+        oracle.set_tie_hook(0, 0.0)

@@ -1,0 +1,62 @@
+"""Aggregate an `ncu --page source --csv --print-source cuda,sass` export (gzip ok) into source
+regions (line ranges per file): share of warp instructions and of stall samples.
+    python tools/ncu_regions.py src.csv.gz"""
+import csv
+import gzip
+import sys
+
+REGIONS = [  # (file, lo, hi, name)
+    ("sample.cuh", 296, 322, "emit/flush"),
+    ("sample.cuh", 323, 338, "load_rec"),
+    ("sample.cuh", 341, 377, "divmod/chunk_log2/exact"),
+    ("sample.cuh", 378, 518, "setup_common (region, ranges, children)"),
+    ("sample.cuh", 519, 872, "setup_job (classify, prefixes, offsets)"),
+    ("sample.cuh", 873, 967, "locate"),
+    ("sample.cuh", 968, 1010, "counters/push_items"),
+    ("sample.cuh", 1011, 1162, "tile/item source"),
+    ("sample.cuh", 1163, 1500, "engine loop"),
+    ("girg_device.cuh", 1, 40, "philox/u53"),
+    ("girg_device.cuh", 41, 115, "morton"),
+    ("girg_device.cuh", 116, 140, "dist/prob"),
+    ("girg_device.cuh", 141, 400, "fast paths"),
+]
+
+
+def region(fn, ln):
+    for f, lo, hi, name in REGIONS:
+        if fn == f and lo <= ln <= hi:
+            return name
+    return fn
+
+
+def main(path):
+    op = gzip.open if path.endswith(".gz") else open
+    agg, cur = {}, None
+    with op(path, "rt") as f:
+        hdr = None
+        for r in csv.reader(f):
+            if len(r) == 2 and r[0] == "File Path":
+                cur = r[1].split("/")[-1]
+                continue
+            if r and r[0] == "Line No":
+                hdr = r
+                continue
+            if hdr is None or not r or not r[0]:
+                continue
+            try:
+                ln, smp, inst = int(r[0]), int(r[4]), int(r[7])
+            except (ValueError, IndexError):
+                continue
+            k = region(cur, ln)
+            a = agg.setdefault(k, [0, 0])
+            a[0] += smp
+            a[1] += inst
+    ts = sum(a[0] for a in agg.values()) or 1
+    ti = sum(a[1] for a in agg.values()) or 1
+    print(f"warp instructions {ti:.3e}, stall samples {ts}")
+    for k, (s, i) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"{100 * i / ti:5.1f}% inst {100 * s / ts:5.1f}% samples  {k}")
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])
