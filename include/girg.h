@@ -136,6 +136,14 @@ typedef struct {
     int scheme;           /* GIRG_SCHEME_MERGED (default) or GIRG_SCHEME_EVENT */
     int shard_level;      /* as girg_edges_shard; 0, [0, 1) = the whole graph */
     uint64_t blk_lo, blk_hi;
+    /* interleaved multi-GPU ownership (nranks > 0; blk_lo / blk_hi are then ignored): an event
+     * whose A cell is on a level l >= shard_level belongs to rank (Morton block of A at
+     * shard_level) mod nranks; a coarser event (l < shard_level) to rank
+     * (A + 7 j + 13 i + 31 l) mod nranks (A its Morton code on level l, (i, j) its layer pair),
+     * so the few large coarse events are spread over the ranks instead of falling to the first
+     * blocks.  The nranks shards of one graph are disjoint and their union is the whole graph.
+     * EINVAL if rank >= nranks.  nranks = 0: block-range mode as girg_edges_shard. */
+    uint32_t nranks, rank;
 } girg_options;
 
 /*

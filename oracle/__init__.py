@@ -82,6 +82,9 @@ def lib():
         L.or_edges.argtypes = [dp, dp, u64, i32, d, d, u64, i32, u64, u64, i32, u32p, u64,
                                C.POINTER(C.c_uint64), C.POINTER(Stats)]
         L.or_edges.restype = i32
+        L.or_edges_ranked.argtypes = [dp, dp, u64, i32, d, d, u64, i32, C.c_uint32, C.c_uint32, i32, u32p, u64,
+                                      C.POINTER(C.c_uint64), C.POINTER(Stats)]
+        L.or_edges_ranked.restype = i32
         L.or_bruteforce_t0.argtypes = [dp, dp, u64, i32, d, u32p, u64, C.POINTER(C.c_uint64)]
         L.or_bruteforce_t0.restype = i32
         L.or_expected_edges_bf.argtypes = [dp, dp, u64, i32, d, d]; L.or_expected_edges_bf.restype = d
@@ -221,9 +224,14 @@ def edges(w, x, d, T, kappa, seed, shard=(0, 0, 1), cap=None, with_stats=False, 
         out = np.empty((cap, 2), dtype=np.uint32)
         m = C.c_uint64(0)
         st = Stats()
-        rc = lib().or_edges(_dp(w), _dp(x), n, d, float(T), float(kappa), C.c_uint64(seed),
-                            shard[0], C.c_uint64(shard[1]), C.c_uint64(shard[2]), scheme, _u32p(out),
-                            cap, C.byref(m), C.byref(st))
+        if len(shard) == 4 and shard[0] == "ranked":  # ("ranked", shard_level, nranks, rank)
+            rc = lib().or_edges_ranked(_dp(w), _dp(x), n, d, float(T), float(kappa), C.c_uint64(seed),
+                                       shard[1], shard[2], shard[3], scheme, _u32p(out), cap, C.byref(m),
+                                       C.byref(st))
+        else:
+            rc = lib().or_edges(_dp(w), _dp(x), n, d, float(T), float(kappa), C.c_uint64(seed),
+                                shard[0], C.c_uint64(shard[1]), C.c_uint64(shard[2]), scheme, _u32p(out),
+                                cap, C.byref(m), C.byref(st))
         if rc == ECAPACITY:
             cap = int(m.value) + 1
             continue

@@ -336,9 +336,10 @@ typedef struct {
     int neq[33], nge[33];
     int eq[33][64 * 65 / 2][2];
     int ge[33][64 * 65 / 2][2];
-    /* shard filter */
+    /* shard filter: block range [blo, bhi) at level sl, or (nranks > 0) interleaved ranks */
     int sl;
     uint64_t blo, bhi;
+    uint32_t nranks, rank;
     /* type-II scheme: OR_SCHEME_EVENT (one jump sequence per distant cell pair, Alg. 1 as
      * written) or OR_SCHEME_MERGED (one sequence per (A cell, bound class), R22) */
     int scheme;
@@ -655,8 +656,26 @@ static uint64_t blk_of(const or_ctx *c, int l, uint32_t A)
     if (l >= c->sl) return (uint64_t)A >> (c->d * (l - c->sl));
     return (uint64_t)A << (c->d * (c->sl - l));
 }
+/* Ownership of the events of A cell A on level l for layer pair (i, j).  Block-range mode: the
+ * block of A (its first descendant's when l < sl) lies in [blo, bhi).  Interleaved mode
+ * (nranks > 0, SURVEY 8(e) "Balance"): rank = block mod nranks for l >= sl; a coarse event
+ * (l < sl) goes to rank (A + 7 j + 13 i + 31 l) mod nranks, so that the few large coarse events
+ * spread over the ranks (unsigned 32-bit arithmetic). */
+static int owns(const or_ctx *c, int l, uint32_t A, int i, int j)
+{
+    if (c->nranks == 0) {
+        uint64_t b = blk_of(c, l, A);
+        return b >= c->blo && b < c->bhi;
+    }
+    uint32_t key = l >= c->sl ? (uint32_t)((uint64_t)A >> (c->d * (l - c->sl)))
+                              : A + 7u * (uint32_t)j + 13u * (uint32_t)i + 31u * (uint32_t)l;
+    return key % c->nranks == c->rank;
+}
+
 static int subtree_may_own(const or_ctx *c, int l, uint32_t A)
 {
+    if (c->nranks > 0) /* interleaved: one block (and rank) per subtree from the split level on */
+        return l < c->sl || (uint32_t)((uint64_t)A >> (c->d * (l - c->sl))) % c->nranks == c->rank;
     if (l >= c->sl) {
         uint64_t b = blk_of(c, l, A);
         return b >= c->blo && b < c->bhi;
@@ -674,25 +693,24 @@ static void recur(or_ctx *c, int l, uint32_t A, uint32_t B)
     if (c->err) return;
     c->st->visits++;
     if (!subtree_may_own(c, l, A)) return;
-    uint64_t b = blk_of(c, l, A);
-    int own = b >= c->blo && b < c->bhi;
     if (or_are_neighbors(A, B, c->d, l)) {
-        if (own)
-            for (int k = 0; k < c->neq[l]; k++) {
-                int i = c->eq[l][k][0], j = c->eq[l][k][1];
-                if (i == j && A > B) continue;
-                type1(c, l, A, B, i, j);
-            }
+        for (int k = 0; k < c->neq[l]; k++) {
+            int i = c->eq[l][k][0], j = c->eq[l][k][1];
+            if (i == j && A > B) continue;
+            if (!owns(c, l, A, i, j)) continue;
+            type1(c, l, A, B, i, j);
+        }
         if (l < c->lv.maxCL) { /* Alg. 1 line 7: refine neighbours until max depth */
             uint32_t nc = 1u << c->d;
             for (uint32_t x = 0; x < nc; x++)
                 for (uint32_t y = 0; y < nc; y++)
                     recur(c, l + 1, (A << c->d) | x, (B << c->d) | y);
         }
-    } else if (c->T > 0.0 && own && c->scheme == OR_SCHEME_EVENT) {
+    } else if (c->T > 0.0 && c->scheme == OR_SCHEME_EVENT) {
         for (int k = 0; k < c->nge[l]; k++) {
             int i = c->ge[l][k][0], j = c->ge[l][k][1];
             if (i == j && A >= B) continue;
+            if (!owns(c, l, A, i, j)) continue;
             type2(c, l, A, B, i, j);
         }
     }
@@ -720,13 +738,13 @@ static void merged_all(or_ctx *c)
             for (uint64_t s = 0; s < ni; s++) {
                 uint32_t A = code[s] >> sh;
                 if (s > 0 && (code[s - 1] >> sh) == A) continue; /* first point of the cell */
-                uint64_t b = blk_of(c, l, A);
-                if (b < c->blo || b >= c->bhi) continue;
+                if (!subtree_may_own(c, l, A)) continue;
                 int n2, n3;
                 distant_cells(c, l, A, l2, &n2, l3, &n3);
                 for (int pr = 0; pr < c->nge[l]; pr++) {
                     if (c->ge[l][pr][0] != i) continue;
                     int j = c->ge[l][pr][1];
+                    if (!owns(c, l, A, i, j)) continue;
                     int s2 = 0, s3 = 0; /* i == j: only B > A (R16); the lists are sorted */
                     if (i == j) {
                         while (s2 < n2 && l2[s2] <= A) s2++;
@@ -761,9 +779,9 @@ static uint64_t now_ns(void)
 }
 
 static int or_run(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
-                  uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi, int scheme,
-                  uint32_t *edges, uint64_t cap, uint64_t *m_out, or_stats_t *st,
-                  uint32_t *cover, or_index_out *ix)
+                  uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi, uint32_t nranks,
+                  uint32_t rank, int scheme, uint32_t *edges, uint64_t cap, uint64_t *m_out,
+                  or_stats_t *st, uint32_t *cover, or_index_out *ix)
 {
     or_stats_t dummy;
     if (!st) st = &dummy;
@@ -773,6 +791,7 @@ static int or_run(const double *w, const double *x, uint64_t n, int d, double T,
     if (!(T >= 0.0 && T < 1.0)) return OR_EINVAL;
     if (!(kappa > 0.0) || !isfinite(kappa)) return OR_EINVAL;
     if (shard_level < 0 || shard_level * d > 32 || blk_lo >= blk_hi) return OR_EINVAL;
+    if (nranks > 0 && rank >= nranks) return OR_EINVAL;
     if (scheme != OR_SCHEME_EVENT && scheme != OR_SCHEME_MERGED) return OR_EINVAL;
     for (uint64_t i = 0; i < (uint64_t)d * n; i++)
         if (!(x[i] >= 0.0 && x[i] < 1.0)) return OR_EINVAL;
@@ -786,6 +805,7 @@ static int or_run(const double *w, const double *x, uint64_t n, int d, double T,
     c->invT = T > 0.0 ? 1.0 / T : 0.0;
     c->s = c->lv.s;
     c->sl = shard_level; c->blo = blk_lo; c->bhi = blk_hi; c->scheme = scheme;
+    c->nranks = nranks; c->rank = rank;
     c->edges = edges; c->cap = cap; c->st = st; c->cover = cover;
     const int L = c->lv.L;
 
@@ -914,7 +934,16 @@ int or_edges(const double *w, const double *x, uint64_t n, int d, double T, doub
              uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi, int scheme,
              uint32_t *edges, uint64_t cap, uint64_t *m_out, or_stats_t *st)
 {
-    return or_run(w, x, n, d, T, kappa, seed, shard_level, blk_lo, blk_hi, scheme, edges, cap,
+    return or_run(w, x, n, d, T, kappa, seed, shard_level, blk_lo, blk_hi, 0, 0, scheme, edges, cap,
+                  m_out, st, NULL, NULL);
+}
+
+int or_edges_ranked(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
+                    uint64_t seed, int shard_level, uint32_t nranks, uint32_t rank, int scheme,
+                    uint32_t *edges, uint64_t cap, uint64_t *m_out, or_stats_t *st)
+{
+    if (nranks == 0) return OR_EINVAL;
+    return or_run(w, x, n, d, T, kappa, seed, shard_level, 0, 1, nranks, rank, scheme, edges, cap,
                   m_out, st, NULL, NULL);
 }
 
@@ -926,7 +955,7 @@ int or_coverage(const double *w, const double *x, uint64_t n, int d, double T, d
     uint64_t m = 0;
     if (!cover || n > 20000) return OR_EINVAL;
     memset(cover, 0, sizeof(uint32_t) * n * n);
-    return or_run(w, x, n, d, T, kappa, 0, 0, 0, 1, scheme, NULL, 0, &m, st, cover, NULL);
+    return or_run(w, x, n, d, T, kappa, 0, 0, 0, 1, 0, 0, scheme, NULL, 0, &m, st, cover, NULL);
 }
 
 int or_index(const double *w, const double *x, uint64_t n, int d, double kappa, uint32_t *order,
@@ -934,7 +963,8 @@ int or_index(const double *w, const double *x, uint64_t n, int d, double kappa, 
 {
     uint64_t m = 0;
     or_index_out ix = {order, lstart, P, poff, pcap};
-    return or_run(w, x, n, d, 0.0, kappa, 0, 0, 0, 1, OR_SCHEME_EVENT, NULL, 0, &m, NULL, NULL, &ix);
+    return or_run(w, x, n, d, 0.0, kappa, 0, 0, 0, 1, 0, 0, OR_SCHEME_EVENT, NULL, 0, &m, NULL, NULL,
+                  &ix);
 }
 
 /* Cell pairs enumerated by Algorithm 1 on a full tree of depth `depth`,

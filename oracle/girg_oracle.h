@@ -94,6 +94,13 @@ int or_edges(const double *w, const double *x, uint64_t n, int d, double T, doub
              uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi, int scheme,
              uint32_t *edges, uint64_t cap, uint64_t *m_out, or_stats_t *st);
 
+/* Interleaved shard ownership (SURVEY 8(e) "Balance"): events whose A cell is on a level
+ * l >= shard_level belong to rank (Morton block at shard_level) mod nranks; coarser events to rank
+ * (A + 7 j + 13 i + 31 l) mod nranks (32-bit unsigned).  The nranks shards partition the graph. */
+int or_edges_ranked(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
+                    uint64_t seed, int shard_level, uint32_t nranks, uint32_t rank, int scheme,
+                    uint32_t *edges, uint64_t cap, uint64_t *m_out, or_stats_t *st);
+
 /* test hooks: instrumented coverage (cover: n*n counters), Lemma-1 index export, and the
  * per-level cell-pair counts of Algorithm 1 on a full tree */
 int or_coverage(const double *w, const double *x, uint64_t n, int d, double T, double kappa,

@@ -42,7 +42,8 @@ class Stats(C.Structure):
 
 
 class Options(C.Structure):
-    _fields_ = [("scheme", C.c_int), ("shard_level", C.c_int), ("blk_lo", C.c_uint64), ("blk_hi", C.c_uint64)]
+    _fields_ = [("scheme", C.c_int), ("shard_level", C.c_int), ("blk_lo", C.c_uint64), ("blk_hi", C.c_uint64),
+                ("nranks", C.c_uint32), ("rank", C.c_uint32)]
 
 
 class Timings(C.Structure):
@@ -180,7 +181,10 @@ def _edges_on_device(w, x, n, d, T, kappa, seed, cap, out, shard, stats, stream,
         buf = out if out is not None else torch.empty((cap, 2), dtype=torch.int32, device=w.device)
         m = C.c_uint64(0)
         st = Stats()
-        opt = Options(scheme, shard[0], shard[1], shard[2])
+        if len(shard) == 4 and shard[0] == "ranked":  # ("ranked", shard_level, nranks, rank)
+            opt = Options(scheme, shard[1], 0, 1, shard[2], shard[3])
+        else:
+            opt = Options(scheme, shard[0], shard[1], shard[2], 0, 0)
         rc = _lib.girg_edges_ex(w.data_ptr(), x.data_ptr(), n, d, T, kappa, seed, C.byref(opt), buf.data_ptr(), cap,
                                 C.byref(m), C.byref(st) if stats else None, _stream(stream))
         if rc == ECAPACITY and out is None:

@@ -949,6 +949,7 @@ struct EdgeCall {
     uint64_t seed;
     int sl;
     uint64_t blo, bhi;
+    uint32_t nranks = 0, rank = 0;  // interleaved ownership (nranks > 0) instead of a block range
     int scheme;
     uint32_t* edges;
     uint64_t cap;
@@ -1112,6 +1113,8 @@ struct EdgeCall {
         a.sl = hp.p.sl;
         a.blo = hp.p.blo;
         a.bhi = hp.p.bhi;
+        a.nranks = nranks;
+        a.rank = rank;
         if (const char* e = getenv("GIRG_DEV_FLAGS")) a.dev_flags = (unsigned)atoi(e);
         PE.record(2, st);
         sample_and_fetch();
@@ -1187,12 +1190,20 @@ struct EdgeCall {
 
 static int edges_impl(const double* w, const double* x, uint64_t n, int d, double T, double kappa,
                       uint64_t seed, int sl, uint64_t blo, uint64_t bhi, int scheme, uint32_t* edges, uint64_t cap,
-                      uint64_t* m_out, girg_stats* stats_out, cudaStream_t st)
+                      uint64_t* m_out, girg_stats* stats_out, cudaStream_t st, uint32_t nranks = 0,
+                      uint32_t rank = 0)
 {
+    if (nranks > 0) {  // interleaved ownership: the block range is unused
+        if (rank >= nranks) return GIRG_EINVAL;
+        blo = 0;
+        bhi = 1;
+    }
     int v = EdgeCall::validate(w, x, n, d, T, kappa, sl, blo, bhi, scheme, edges, cap, m_out);
     if (v != GIRG_OK) return v;
     try {
         EdgeCall E(w, x, n, d, T, kappa, seed, sl, blo, bhi, scheme, edges, cap, m_out, stats_out, st);
+        E.nranks = nranks;
+        E.rank = rank;
         E.stage_a();
         GCHECK(cudaStreamSynchronize(st));
         E.stage_b();
@@ -1506,10 +1517,10 @@ extern "C" int girg_edges_ex(const double* w_dev, const double* x_dev, uint64_t 
                              uint64_t seed, const girg_options* opt, uint32_t* edges_dev, uint64_t cap,
                              uint64_t* m_out, girg_stats* stats_out, void* stream)
 {
-    girg_options o = {GIRG_SCHEME_MERGED, 0, 0, 1};
+    girg_options o = {GIRG_SCHEME_MERGED, 0, 0, 1, 0, 0};
     if (opt) o = *opt;
     return edges_impl(w_dev, x_dev, n, d, T, kappa, seed, o.shard_level, o.blk_lo, o.blk_hi, o.scheme, edges_dev, cap,
-                      m_out, stats_out, (cudaStream_t)stream);
+                      m_out, stats_out, (cudaStream_t)stream, o.nranks, o.rank);
 }
 
 extern "C" int girg_edges_host(const double* w_host, const double* x_host, uint64_t n, int d, double T,

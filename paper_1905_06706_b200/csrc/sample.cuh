@@ -191,6 +191,7 @@ struct SampleArgs {
     double T, s, invT;
     int sl;
     unsigned long long blo, bhi;
+    uint32_t nranks, rank;  // interleaved ownership (nranks > 0), else the block range [blo, bhi)
 };
 
 struct TaskDesc {
@@ -402,6 +403,25 @@ struct JobSetup {
     int nseq2;                // nonempty type-II sequences (counter)
 };
 
+// Shard ownership of the events whose A cell (the job child) is A on level l, layer pair (i, j)
+// (DESIGN.md "Multi-GPU").  Block range mode (nranks = 0): the Morton block of A at
+// the split level sl in [blo, bhi) (a coarser A: the block of its first descendant).
+// Interleaved mode (nranks > 0): rank = block mod nranks for l >= sl, and for the coarse events
+// (l < sl, which would all fall to a few first-descendant blocks) rank = (A + 7 j + 13 i + 31 l)
+// mod nranks, spreading them by identity.
+template <int D>
+__device__ __forceinline__ bool owns(const SampleArgs& a, uint32_t A, int l, int i, int j)
+{
+    if (a.nranks == 0) {
+        const unsigned long long b = l >= a.sl ? ((unsigned long long)A >> (D * (l - a.sl)))
+                                               : ((unsigned long long)A << (D * (a.sl - l)));
+        return b >= a.blo && b < a.bhi;
+    }
+    const uint32_t key = l >= a.sl ? (uint32_t)((unsigned long long)A >> (D * (l - a.sl)))
+                                   : A + 7u * (uint32_t)j + 13u * (uint32_t)i + 31u * (uint32_t)l;
+    return key % a.nranks == a.rank;
+}
+
 // ---- job setup, common part (warp-collective): region parents in Morton order, the Lemma-1
 // ranges of their sub-cells (layer j) and of the task cell's children (layer i), the nonempty
 // owned children of this batch, the job constants.  Returns the batch's child count.
@@ -485,9 +505,7 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
             if (e < nsub) {
                 ok = S.achild[e + 1] > S.achild[e];
                 const uint32_t A = (t.Cpar << t.cs) + (uint32_t)e;
-                const unsigned long long b = t.l >= a.sl ? ((unsigned long long)A >> (D * (t.l - a.sl)))
-                                                         : ((unsigned long long)A << (D * (a.sl - t.l)));
-                ok = ok && b >= a.blo && b < a.bhi;
+                ok = ok && owns<D>(a, A, t.l, t.i, t.j);
             }
             const unsigned bm = __ballot_sync(FULL, ok);
             const int rank = cnt + __popc(bm & ((1u << lane) - 1u));

@@ -364,3 +364,27 @@ def test_crowded_cell_linear_order(d, T, nc, kappa):
         x[k, idx] = 0.5 + rng.integers(0, 1 << 20, size=idx.size) * 2.0**-53  # width 1.2e-10
     g, st, so = assert_parity(w, x, d, T, kappa, 3)
     assert len(g) > 1000
+
+
+@pytest.mark.parametrize("d,T,scheme", [(2, 0.8, girg.SCHEME_MERGED), (3, 0.9, girg.SCHEME_MERGED),
+                                        (1, 0.5, girg.SCHEME_EVENT)])
+def test_ranked_shards_equal_oracle_and_union(d, T, scheme):
+    """Interleaved multi-GPU ownership (girg_options.nranks, sharding.shard_for_rank): every rank's
+    shard equals the oracle's shard of the same rank, and the N shards partition the full graph."""
+    from paper_1905_06706_b200.sharding import shard_for_rank
+
+    n = 40_000
+    w, x = synth_inputs(n, d, 2.4, 70 + d)
+    kappa = O.scale_weights(w, 12.0, d, T, 2.4)
+    wd, xd = dev(w), dev(x)
+    full = gpu_keys(girg.edges(wd, xd, T, kappa, 4, scheme=scheme))
+    world = 3
+    parts = []
+    for r in range(world):
+        sh = shard_for_rank(d, world, r)
+        g = gpu_keys(girg.edges(wd, xd, T, kappa, 4, shard=sh, scheme=scheme))
+        eo, so = O.edges(w, x, d, T, kappa, 4, shard=sh, with_stats=True, scheme=scheme)
+        assert so["nt1"] + so["nt2acc"] + so["nt2jump"] == 0
+        assert np.array_equal(g, O.sort_edges(eo)), r
+        parts.append(g)
+    assert np.array_equal(np.sort(np.concatenate(parts)), full)

@@ -24,7 +24,7 @@ def free_port():
     return p
 
 
-def worker(rank, world, port, d, T, q):
+def worker(rank, world, port, d, T, q, mode="ranked"):
     import sys
 
     sys.path.insert(0, ROOT)
@@ -37,7 +37,7 @@ def worker(rank, world, port, d, T, q):
     n = 6000
     w, x = synth_inputs(n, d, 2.4, 90 + d)
     kappa = oracle.scale_weights(w, 10.0, d, T, 2.4)
-    e = oracle.edges(w, x, d, T, kappa, 11, shard=shard_for_rank(d, world, rank))
+    e = oracle.edges(w, x, d, T, kappa, 11, shard=shard_for_rank(d, world, rank, mode=mode))
     keys = oracle.sort_edges(e).astype(np.int64)
     cnt = torch.tensor([len(keys)], dtype=torch.int64)
     counts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
@@ -55,12 +55,13 @@ def worker(rank, world, port, d, T, q):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("mode", ["ranked", "range"])
 @pytest.mark.parametrize("d,T", [(1, 0.5), (2, 0.8), (3, 0.0)])
-def test_two_rank_shards_cover_the_graph(d, T):
+def test_two_rank_shards_cover_the_graph(d, T, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, 2, port, d, T, q)) for r in range(2)]
+    procs = [ctx.Process(target=worker, args=(r, 2, port, d, T, q, mode)) for r in range(2)]
     for p in procs:
         p.start()
     total, counts, m_full, equal, disjoint = q.get(timeout=300)
@@ -77,7 +78,9 @@ def test_shard_ranges_partition_blocks():
 
     for d in (1, 2, 3, 5):
         for world in (1, 2, 3, 4, 8):
-            rs = [shard_for_rank(d, world, r) for r in range(world)]
+            assert [shard_for_rank(d, world, r)[2:] for r in range(world) if world > 1] == \
+                [(world, r) for r in range(world) if world > 1]
+            rs = [shard_for_rank(d, world, r, mode="range") for r in range(world)]
             if world == 1:
                 assert rs == [(0, 0, 1)]
                 continue
@@ -86,3 +89,28 @@ def test_shard_ranges_partition_blocks():
             assert rs[0][1] == 0 and rs[-1][2] == 1 << (d * sl)
             assert all(a[2] == b[1] for a, b in zip(rs, rs[1:]))
             assert (1 << (d * sl)) >= 64 * world or d * (sl + 1) > 30
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_ranked_shards_partition_and_spread_coarse_events(scheme):
+    """Interleaved ownership (SURVEY 8(e) "Balance"), oracle only: for N = 3 and 4 the shards are
+    disjoint, their union is the full edge set, and no rank is starved or overloaded -- the
+    coarse events (levels below the split level) are spread by identity, not given to rank 0."""
+    import sys
+
+    sys.path.insert(0, ROOT)
+    import oracle
+    from paper_1905_06706_b200.sharding import shard_for_rank
+    from workloads import synth_inputs
+
+    n, d, T = 8000, 2, 0.7
+    w, x = synth_inputs(n, d, 2.3, 17)
+    kappa = oracle.scale_weights(w, 12.0, d, T, 2.3)
+    full = oracle.sort_edges(oracle.edges(w, x, d, T, kappa, 5, scheme=scheme))
+    for world in (3, 4):
+        parts = [oracle.sort_edges(oracle.edges(w, x, d, T, kappa, 5, shard=shard_for_rank(d, world, r),
+                                                scheme=scheme)) for r in range(world)]
+        union = np.sort(np.concatenate(parts))
+        assert np.array_equal(union, full)
+        sizes = [len(p) for p in parts]
+        assert max(sizes) < 1.25 * min(sizes), sizes
