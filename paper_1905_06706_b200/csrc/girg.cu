@@ -11,6 +11,7 @@
 //                   jumps (Algorithm 1 events), warp-staged edge output; k_big runs
 //                   the unit ranges of queued big jobs (csrc/sample.cuh)
 // Citations "P:NNN" are lines of PAPER.md (arXiv:1905.06706); R* are DESIGN.md readings.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -597,33 +598,42 @@ struct Scratch {
 static inline unsigned grid_for(uint64_t n, unsigned threads) { return (unsigned)((n + threads - 1) / threads); }
 
 // round a 256-bit non-negative integer (4 x u64, little endian) times 2^e2 to double (RNE)
-static double round_u256(const unsigned long long a[4], int e2)
+__host__ __device__ inline int clz64(unsigned long long x)
+{
+#ifdef __CUDA_ARCH__
+    return __clzll((long long)x);
+#else
+    return __builtin_clzll(x);
+#endif
+}
+
+__host__ __device__ inline double round_u256(const unsigned long long a[4], int e2)
 {
     int top = -1;
     for (int k = 3; k >= 0 && top < 0; --k)
-        if (a[k]) top = 64 * k + 63 - __builtin_clzll(a[k]);
+        if (a[k]) top = 64 * k + 63 - clz64(a[k]);
     if (top < 0) return 0.0;
-    auto bit = [&](int i) -> unsigned { return i < 0 ? 0u : (unsigned)((a[i / 64] >> (i % 64)) & 1ull); };
     unsigned long long mant = 0;
-    const int lo = std::max(0, top - 52);
-    for (int b = top; b >= lo; --b) mant = (mant << 1) | bit(b);
-    if (top <= 52) return std::ldexp((double)mant, e2);
-    const unsigned rnd = bit(top - 53);
+    const int lo = top - 52 > 0 ? top - 52 : 0;
+    for (int b = top; b >= lo; --b) mant = (mant << 1) | ((a[b / 64] >> (b % 64)) & 1ull);
+    if (top <= 52) return ldexp((double)mant, e2);
+    const unsigned rnd = (unsigned)((a[(top - 53) / 64] >> ((top - 53) % 64)) & 1ull);
     bool sticky = false;
-    for (int b = top - 54; b >= 0 && !sticky; --b) sticky = bit(b) != 0;
+    for (int b = top - 54; b >= 0 && !sticky; --b) sticky = ((a[b / 64] >> (b % 64)) & 1ull) != 0;
     int t = top;
     if (rnd && (sticky || (mant & 1ull))) {
         ++mant;
         if (mant == (1ull << 53)) { mant >>= 1; ++t; }
     }
-    return std::ldexp((double)mant, t - 52 + e2);
+    return ldexp((double)mant, t - 52 + e2);
 }
 
 // exact W = sum_b part_b * 2^(e_b - 52), rounded once (R3)
-static double exact_W(const std::vector<WPartial>& parts, int emin)
+__host__ __device__ inline double exact_W(const WPartial* parts, size_t nparts, int emin)
 {
     unsigned long long acc[4] = {0, 0, 0, 0};
-    for (const WPartial& q : parts) {
+    for (size_t b = 0; b < nparts; ++b) {
+        const WPartial& q = parts[b];
         if (q.e_b == INT_MAX) continue;  // empty block
         const int sh = q.e_b - emin;       // 0..63
         unsigned long long v[4] = {0, 0, 0, 0};
@@ -646,6 +656,7 @@ static double exact_W(const std::vector<WPartial>& parts, int emin)
     }
     return round_u256(acc, emin - 52);
 }
+static double exact_W(const std::vector<WPartial>& parts, int emin) { return exact_W(parts.data(), parts.size(), emin); }
 
 struct HostPlan {
     Plan p;
@@ -775,28 +786,6 @@ static int map_cuda(cudaError_t e)
 {
     g_last_cuda = cudaGetErrorString(e);
     return e == cudaErrorMemoryAllocation ? GIRG_ENOMEM : GIRG_ECUDA;
-}
-
-// K0 on the device + D2H of the histogram and partials (one synchronisation)
-static void run_wstats(const double* w, uint64_t n, cudaStream_t st, Scratch& S, std::vector<uint32_t>& hist,
-                       std::vector<WPartial>& parts, int& err_host)
-{
-    const unsigned nb = grid_for(n, WS_TILE);
-    const size_t bytes = HIST_BINS * sizeof(uint32_t) + nb * sizeof(WPartial) + 16;
-    char* buf = S.alloc<char>(bytes);
-    uint32_t* d_hist = (uint32_t*)buf;
-    int* d_err = (int*)(buf + HIST_BINS * sizeof(uint32_t));
-    WPartial* d_part = (WPartial*)(buf + HIST_BINS * sizeof(uint32_t) + 16);
-    GCHECK(cudaMemsetAsync(buf, 0, HIST_BINS * sizeof(uint32_t) + 16, st));
-    k_wstats<<<nb, WS_THREADS, 0, st>>>(w, (uint32_t)n, d_hist, d_part, d_err);
-    GCHECK(cudaGetLastError());
-    std::vector<char> h(bytes);
-    GCHECK(cudaMemcpyAsync(h.data(), buf, bytes, cudaMemcpyDeviceToHost, st));
-    GCHECK(cudaStreamSynchronize(st));
-    hist.assign((uint32_t*)h.data(), (uint32_t*)h.data() + HIST_BINS);
-    std::memcpy(&err_host, h.data() + HIST_BINS * sizeof(uint32_t), sizeof(int));
-    parts.resize(nb);
-    std::memcpy(parts.data(), h.data() + HIST_BINS * sizeof(uint32_t) + 16, nb * sizeof(WPartial));
 }
 
 // SM count of the current device (queried once per device)
@@ -1227,110 +1216,84 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
 // heavier candidates; host: the monotone search on f with E_R evaluated in O(|R|) over the
 // sorted candidates (same decomposition as DESIGN.md R12).
 // ======================================================================================
-constexpr int SUM_THREADS = 256;
-
+// One cooperative launch (grid-wide barriers), one synchronisation for the caller:
+//   1  global e_min / w_max / input checks;  2  exact W (192-bit per-thread fixed point relative
+//   to e_min, block partials summed in 256 bits by block 0 and rounded once, R3);  3  kappa0,
+//   a0 = 2^d kappa0 / W and the tail threshold tau = 1/(64 a0 w_max): vertices with w <= tau are
+//   never saturated for kappa <= 64 kappa0, so their power sums (sum w, w^2, (w/wmax)^(1/T),
+//   (w/wmax)^(2/T)) are kappa-independent and summed once; heavier vertices are compacted;
+//   4  block 0 sorts the candidates (bitonic), forms suffix sums, and runs the exponential
+//   search + bisection on f with E_R in O(|R|) per evaluation (same decomposition as the
+//   oracle's or_f, R12).  The host re-launches only if the candidate buffer is too
+//   small or the search leaves the range covered by tau (status codes below).
+constexpr int SC_THREADS = 256;
+struct Acc192 {
+    unsigned long long v[3];
+};
 struct TailSums {
     double s1, s2, z1, z2;  // sum w, sum w^2, sum (w/wmax)^(1/T), sum (w/wmax)^(2/T) over w <= tau
 };
+struct ScaleCtl {
+    int emin;               // global minimum exponent (atomicMin)
+    int err;                // ERR_WEIGHT / ERR_WRANGE
+    unsigned long long wmax_bits;
+    unsigned int ncand;     // candidates (w > tau) seen
+    int status;             // 0 ok, 1 candidate buffer too small, 2 tau too large for a kappa, 3 range
+    double W, wmax, tau, kappa;
+};
+constexpr int SC_OK = 0, SC_CAP = 1, SC_TAU = 2, SC_RANGE = 3;
 
-__global__ void __launch_bounds__(SUM_THREADS) k_wsums(const double* __restrict__ w, uint32_t n, double tau,
-                                                       double wmax, double invT, TailSums* __restrict__ part,
-                                                       double* __restrict__ cand, uint32_t* __restrict__ ncand,
-                                                       uint32_t cap)
+__device__ __forceinline__ void add192(Acc192& a, unsigned long long lo, unsigned long long hi)
 {
-    __shared__ double sh[4][SUM_THREADS / 32];
-    double a1 = 0, a2 = 0, b1 = 0, b2 = 0;
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        const double wv = w[v];
-        if (wv <= tau) {
-            a1 += wv;
-            a2 += wv * wv;
-            if (invT > 0.0) {
-                const double z = pow(wv / wmax, invT);
-                b1 += z;
-                b2 += z * z;
-            }
-        } else {
-            const uint32_t k = atomicAdd(ncand, 1u);
-            if (k < cap) cand[k] = wv;
-        }
-    }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-        a1 += __shfl_down_sync(0xffffffffu, a1, off);
-        a2 += __shfl_down_sync(0xffffffffu, a2, off);
-        b1 += __shfl_down_sync(0xffffffffu, b1, off);
-        b2 += __shfl_down_sync(0xffffffffu, b2, off);
-    }
-    const int wid = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0) { sh[0][wid] = a1; sh[1][wid] = a2; sh[2][wid] = b1; sh[3][wid] = b2; }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        TailSums t = {0, 0, 0, 0};
-        for (int k = 0; k < SUM_THREADS / 32; ++k) { t.s1 += sh[0][k]; t.s2 += sh[1][k]; t.z1 += sh[2][k]; t.z2 += sh[3][k]; }
-        part[blockIdx.x] = t;
-    }
+    const unsigned long long t0 = a.v[0] + lo;
+    const unsigned long long c0 = t0 < lo;
+    const unsigned long long t1 = a.v[1] + hi;
+    const unsigned long long c1 = t1 < hi;
+    const unsigned long long t1b = t1 + c0;
+    const unsigned long long c1b = t1b < t1;
+    a.v[0] = t0;
+    a.v[1] = t1b;
+    a.v[2] += c1 + c1b;
+}
+__device__ __forceinline__ void add192(Acc192& a, const Acc192& b)
+{
+    add192(a, b.v[0], b.v[1]);
+    a.v[2] += b.v[2];
 }
 
-struct Estimator {
+// f(kappa) over the sorted candidates (decreasing) and the tail sums; false if kappa is outside
+// the range covered by tau (R must lie inside the candidates) or f is not finite
+struct DevEstimator {
     uint64_t n;
     int d;
     double T, W, wmax, tau;
-    TailSums tail;                // fixed-order sum of the block partials
-    std::vector<double> cand;     // weights > tau, decreasing
-    std::vector<double> zeta;     // (cand / wmax)^(1/T), computed once per tau (set_cand)
-    std::vector<double> sc1, sc2, sz1, sz2;  // suffix sums of cand, cand^2, zeta, zeta^2 (from k on)
-    mutable std::vector<double> S1s, SPs;  // scratch of f (no allocation per evaluation)
+    TailSums tail;
+    const double *cand, *zeta, *sc1, *sc2, *sz1, *sz2;
+    double *S1s, *SPs;
+    uint32_t nc;
 
-    void set_cand()
+    __device__ bool f(double kappa, double& out) const
     {
-        const double invT = T > 0.0 ? 1.0 / T : 0.0;
-        const size_t nc = cand.size();
-        zeta.resize(nc);
-        for (size_t k = 0; k < nc; ++k) zeta[k] = T > 0.0 ? std::pow(cand[k] / wmax, invT) : 0.0;
-        sc1.assign(nc + 1, 0.0);
-        sc2.assign(nc + 1, 0.0);
-        sz1.assign(nc + 1, 0.0);
-        sz2.assign(nc + 1, 0.0);
-        for (size_t k = nc; k-- > 0;) {  // ascending weights: small terms first
-            sc1[k] = sc1[k + 1] + cand[k];
-            sc2[k] = sc2[k + 1] + cand[k] * cand[k];
-            sz1[k] = sz1[k + 1] + zeta[k];
-            sz2[k] = sz2[k + 1] + zeta[k] * zeta[k];
-        }
-    }
-
-    // f(kappa); returns false if tau is not small enough for this kappa (R must lie in cand)
-    bool f(double kappa, double& out) const
-    {
-        const double a = std::ldexp(kappa, d) / W;
+        const double a = ldexp(kappa, d) / W;
         if ((a * tau) * wmax > 1.0) return false;
         const double invT = T > 0.0 ? 1.0 / T : 0.0;
-        const double G = T > 0.0 ? std::pow(std::sqrt(a) * wmax, invT) : 0.0;
-        const size_t nc = cand.size();
-        // R = prefix of cand with (a w) wmax > 1
-        size_t nr = 0;
+        const double G = T > 0.0 ? pow(sqrt(a) * wmax, invT) : 0.0;
+        uint32_t nr = 0;  // R = prefix of cand with (a w) wmax > 1
         while (nr < nc && (a * cand[nr]) * wmax > 1.0) ++nr;
-        if (S1s.size() < nr + 1) {
-            S1s.resize(nr + 1);
-            SPs.resize(nr + 1);
-        }
-        // candidates outside R (suffix sums, O(1) per evaluation)
         const double Wsmall = tail.s1 + sc1[nr], Zs = tail.z1 + sz1[nr], W2s = tail.s2 + sc2[nr],
                      Z2s = tail.z2 + sz2[nr];
         S1s[nr] = 0.0;
         SPs[nr] = 0.0;
-        for (size_t k = nr; k-- > 0;) {
+        for (uint32_t k = nr; k-- > 0;) {
             S1s[k] = S1s[k + 1] + cand[k];
             SPs[k] = SPs[k + 1] + zeta[k];
         }
         const double Wt = Wsmall + S1s[0], Zt = Zs + SPs[0];
-        // pairs (u outside R, any v != u): all non-E_R
-        double Lsum = Wt * Wsmall - W2s;
-        double Psum = Zt * Zs - Z2s;  // in units of G^2
+        double Lsum = Wt * Wsmall - W2s;  // pairs (u outside R, any v != u): all non-E_R
+        double Psum = Zt * Zs - Z2s;      // in units of G^2
         double nER = 0.0;
-        size_t m = nr;
-        for (size_t t = 0; t < nr; ++t) {
+        uint32_t m = nr;
+        for (uint32_t t = 0; t < nr; ++t) {
             while (m > 0 && !((a * cand[t]) * cand[m - 1] > 1.0)) --m;
             const bool self = t < m;
             nER += (double)(m - (self ? 1 : 0));
@@ -1339,45 +1302,220 @@ struct Estimator {
         }
         const double tot = T == 0.0 ? a * Lsum + nER : (a * Lsum - T * (G * G) * Psum) / (1.0 - T) + nER;
         out = tot / (double)n;
-        return std::isfinite(out);
+        return isfinite(out);
     }
 };
 
-static void estimator_tail(const double* w, uint64_t n, Estimator& E, cudaStream_t st)
+__global__ void __launch_bounds__(SC_THREADS) k_scale(const double* __restrict__ w, uint32_t n, int d, double T,
+                                                      double avg_deg, double beta, double tau_in,
+                                                      Acc192* __restrict__ wpart, TailSums* __restrict__ tpart,
+                                                      double* __restrict__ scr, uint32_t cap, ScaleCtl* ctl)
 {
-    uint32_t cap = 1u << 16;
-    for (;;) {
-        Scratch S(st);
-        const unsigned nb = std::min<unsigned>(grid_for(n, SUM_THREADS), (unsigned)device_sms() * 8u);
-        TailSums* d_part = S.alloc<TailSums>(nb);
-        double* d_cand = S.alloc<double>(cap);
-        uint32_t* d_nc = S.alloc<uint32_t>(1);
-        GCHECK(cudaMemsetAsync(d_nc, 0, sizeof(uint32_t), st));
-        k_wsums<<<nb, SUM_THREADS, 0, st>>>(w, (uint32_t)n, E.tau, E.wmax, E.T > 0.0 ? 1.0 / E.T : 0.0, d_part,
-                                            d_cand, d_nc, cap);
-        GCHECK(cudaGetLastError());
-        std::vector<TailSums> hp(nb);
-        uint32_t nc = 0;
-        GCHECK(cudaMemcpyAsync(hp.data(), d_part, nb * sizeof(TailSums), cudaMemcpyDeviceToHost, st));
-        GCHECK(cudaMemcpyAsync(&nc, d_nc, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        GCHECK(cudaStreamSynchronize(st));
-        if (nc > cap) {
-            cap = nc;
-            continue;
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const unsigned tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+    const size_t gtid = (size_t)blockIdx.x * blockDim.x + tid, gstride = (size_t)gridDim.x * blockDim.x;
+    __shared__ Acc192 sh_a[SC_THREADS / 32];
+    __shared__ double sh_t[4][SC_THREADS / 32];
+    // ---- 1: e_min, w_max, input checks ----
+    {
+        int emin = INT_MAX, bad = 0;
+        unsigned long long wmb = 0;
+        for (size_t v = gtid; v < n; v += gstride) {
+            const unsigned long long bits = __double_as_longlong(w[v]);
+            const int ef = (int)((bits >> 52) & 0x7ff);
+            if ((bits >> 63) || ef == 0 || ef == 0x7ff) { bad |= ERR_WEIGHT; continue; }
+            emin = min(emin, ef - EXP_BIAS);
+            wmb = max(wmb, bits);
         }
-        E.cand.resize(nc);
-        if (nc) {
-            GCHECK(cudaMemcpyAsync(E.cand.data(), d_cand, nc * sizeof(double), cudaMemcpyDeviceToHost, st));
-            GCHECK(cudaStreamSynchronize(st));
+        for (int o = 16; o; o >>= 1) {
+            emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+            wmb = max(wmb, __shfl_xor_sync(0xffffffffu, wmb, o));
+            bad |= __shfl_xor_sync(0xffffffffu, bad, o);
         }
-        std::sort(E.cand.begin(), E.cand.end(), [](double x, double y) { return x > y; });
-        E.set_cand();
-        E.tail = TailSums{0, 0, 0, 0};
-        for (const TailSums& t : hp) {
-            E.tail.s1 += t.s1; E.tail.s2 += t.s2; E.tail.z1 += t.z1; E.tail.z2 += t.z2;
+        if (lane == 0) {
+            atomicMin(&ctl->emin, emin);
+            atomicMax(&ctl->wmax_bits, wmb);
+            if (bad) atomicOr(&ctl->err, bad);
         }
+    }
+    grid.sync();
+    const int emin = ctl->emin;
+    // ---- 2: exact W partials (192-bit per thread, relative to the global e_min) ----
+    {
+        Acc192 acc = {{0, 0, 0}};
+        int bad = 0;
+        for (size_t v = gtid; v < n; v += gstride) {
+            const unsigned long long bits = __double_as_longlong(w[v]);
+            const int ef = (int)((bits >> 52) & 0x7ff);
+            if ((bits >> 63) || ef == 0 || ef == 0x7ff) continue;
+            const int sh = ef - EXP_BIAS - emin;
+            if (sh > 63) { bad = ERR_WRANGE; continue; }
+            const unsigned long long m = (bits & ((1ull << 52) - 1)) | (1ull << 52);
+            add192(acc, m << sh, sh ? (m >> (64 - sh)) : 0ull);
+        }
+        if (bad) atomicOr(&ctl->err, bad);
+        for (int o = 16; o; o >>= 1) {
+            Acc192 b;
+            for (int k = 0; k < 3; ++k) b.v[k] = __shfl_down_sync(0xffffffffu, acc.v[k], o);
+            add192(acc, b);
+        }
+        if (lane == 0) sh_a[wid] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            Acc192 t = {{0, 0, 0}};
+            for (int k = 0; k < SC_THREADS / 32; ++k) add192(t, sh_a[k]);
+            wpart[blockIdx.x] = t;
+        }
+    }
+    grid.sync();
+    // ---- 3: W, kappa0, tau (block 0, thread 0) ----
+    if (blockIdx.x == 0 && tid == 0) {
+        unsigned long long acc4[4] = {0, 0, 0, 0};
+        for (unsigned b = 0; b < gridDim.x; ++b) {
+            const Acc192& q = wpart[b];
+            unsigned long long carry = 0;
+            for (int k = 0; k < 4; ++k) {
+                const unsigned long long add = k < 3 ? q.v[k] : 0ull;
+                const unsigned long long s1 = acc4[k] + add;
+                const unsigned long long c1 = s1 < acc4[k];
+                const unsigned long long s2 = s1 + carry;
+                const unsigned long long c2 = s2 < s1;
+                acc4[k] = s2;
+                carry = c1 + c2;
+            }
+        }
+        ctl->W = round_u256(acc4, emin - 52);
+        ctl->wmax = __longlong_as_double((long long)ctl->wmax_bits);
+        const double Ew = (beta - 1.0) / (beta - 2.0);
+        const double k0 = avg_deg * (1.0 - T) / (ldexp(1.0, d) * Ew);
+        ctl->kappa = k0;
+        const double a0 = ldexp(k0, d) / ctl->W;
+        ctl->tau = tau_in > 0.0 ? tau_in : 1.0 / (64.0 * a0 * ctl->wmax);
+        ctl->ncand = 0;
+    }
+    grid.sync();
+    if (ctl->err) return;
+    const double tau = ctl->tau, wmax = ctl->wmax, invT = T > 0.0 ? 1.0 / T : 0.0;
+    double* cand = scr;  // [cap2] candidates, then the sort / suffix arrays
+    // ---- 4: tail power sums (fixed-order per thread / warp / block) and candidates ----
+    {
+        double a1 = 0, a2 = 0, b1 = 0, b2 = 0;
+        for (size_t v = gtid; v < n; v += gstride) {
+            const double wv = w[v];
+            if (wv <= tau) {
+                a1 += wv;
+                a2 += wv * wv;
+                if (invT > 0.0) {
+                    const double z = pow(wv / wmax, invT);
+                    b1 += z;
+                    b2 += z * z;
+                }
+            } else {
+                const uint32_t k = atomicAdd(&ctl->ncand, 1u);
+                if (k < cap) cand[k] = wv;
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            a1 += __shfl_down_sync(0xffffffffu, a1, o);
+            a2 += __shfl_down_sync(0xffffffffu, a2, o);
+            b1 += __shfl_down_sync(0xffffffffu, b1, o);
+            b2 += __shfl_down_sync(0xffffffffu, b2, o);
+        }
+        if (lane == 0) { sh_t[0][wid] = a1; sh_t[1][wid] = a2; sh_t[2][wid] = b1; sh_t[3][wid] = b2; }
+        __syncthreads();
+        if (tid == 0) {
+            TailSums t = {0, 0, 0, 0};
+            for (int k = 0; k < SC_THREADS / 32; ++k) { t.s1 += sh_t[0][k]; t.s2 += sh_t[1][k]; t.z1 += sh_t[2][k]; t.z2 += sh_t[3][k]; }
+            tpart[blockIdx.x] = t;
+        }
+    }
+    grid.sync();
+    if (blockIdx.x != 0) return;
+    // ---- 5: block 0: sort, suffix sums, search ----
+    const uint32_t nc = ctl->ncand;
+    if (nc > cap) {
+        if (tid == 0) ctl->status = SC_CAP;
         return;
     }
+    uint32_t n2 = 1;
+    while (n2 < nc) n2 <<= 1;
+    for (uint32_t k = nc + tid; k < n2; k += SC_THREADS) cand[k] = -1.0;  // padding sorts last
+    __syncthreads();
+    for (uint32_t size = 2; size <= n2; size <<= 1)  // bitonic sort, decreasing
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = tid; i < n2 / 2; i += SC_THREADS) {
+                const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                const bool desc = (lo & size) == 0;
+                const double x = cand[lo], y = cand[hi];
+                if ((x < y) == desc) { cand[lo] = y; cand[hi] = x; }
+            }
+            __syncthreads();
+        }
+    double* zeta = cand + n2;
+    double* sc1 = zeta + n2;
+    double* sc2 = sc1 + n2 + 1;
+    double* sz1 = sc2 + n2 + 1;
+    double* sz2 = sz1 + n2 + 1;
+    double* S1s = sz2 + n2 + 1;
+    double* SPs = S1s + n2 + 1;
+    for (uint32_t k = tid; k < nc; k += SC_THREADS) zeta[k] = T > 0.0 ? pow(cand[k] / wmax, invT) : 0.0;
+    __syncthreads();
+    if (tid != 0) return;
+    sc1[nc] = sc2[nc] = sz1[nc] = sz2[nc] = 0.0;
+    for (uint32_t k = nc; k-- > 0;) {  // ascending weights: small terms first
+        sc1[k] = sc1[k + 1] + cand[k];
+        sc2[k] = sc2[k + 1] + cand[k] * cand[k];
+        sz1[k] = sz1[k + 1] + zeta[k];
+        sz2[k] = sz2[k + 1] + zeta[k] * zeta[k];
+    }
+    DevEstimator E;
+    E.n = n;
+    E.d = d;
+    E.T = T;
+    E.W = ctl->W;
+    E.wmax = wmax;
+    E.tau = tau;
+    E.tail = TailSums{0, 0, 0, 0};
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+        E.tail.s1 += tpart[b].s1; E.tail.s2 += tpart[b].s2; E.tail.z1 += tpart[b].z1; E.tail.z2 += tpart[b].z2;
+    }
+    E.cand = cand; E.zeta = zeta; E.sc1 = sc1; E.sc2 = sc2; E.sz1 = sz1; E.sz2 = sz2;
+    E.S1s = S1s; E.SPs = SPs; E.nc = nc;
+    double fv, lo, hi;
+    const double k0 = ctl->kappa;
+    auto fail_tau = [&](double kappa) { ctl->status = SC_TAU; ctl->kappa = kappa; };
+    if (!E.f(k0, fv)) { fail_tau(k0); return; }
+    int it = 0;
+    if (fv < avg_deg) {
+        lo = k0;
+        hi = 2.0 * k0;
+        for (;;) {
+            if (!E.f(hi, fv)) { fail_tau(hi); return; }
+            if (!(fv < avg_deg)) break;
+            lo = hi;
+            hi *= 2.0;
+            if (++it > 2000) { ctl->status = SC_RANGE; return; }
+        }
+    } else {
+        hi = k0;
+        lo = 0.5 * k0;
+        for (;;) {
+            if (!E.f(lo, fv)) { fail_tau(lo); return; }
+            if (fv < avg_deg) break;
+            hi = lo;
+            lo *= 0.5;
+            if (++it > 2000) { ctl->status = SC_RANGE; return; }
+        }
+    }
+    for (it = 0; it < 200 && hi / lo - 1.0 >= 1e-13; ++it) {
+        const double mid = sqrt(lo * hi);
+        if (!E.f(mid, fv)) { fail_tau(mid); return; }
+        if (fv < avg_deg) lo = mid;
+        else hi = mid;
+    }
+    ctl->kappa = 0.5 * (lo + hi);
+    ctl->status = SC_OK;
 }
 
 static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double T, double beta, double* kappa_out,
@@ -1387,74 +1525,53 @@ static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double
     if (!(T >= 0.0 && T < 1.0) || !(beta > 2.0) || !std::isfinite(beta)) return GIRG_EINVAL;
     if (!(avg_deg > 0.0 && avg_deg < (double)(n - 1))) return GIRG_EINVAL;
     try {
-        Estimator E;
-        E.n = n;
-        E.d = d;
-        E.T = T;
-        {
+        static int occ = [] {
+            int v = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_scale, SC_THREADS, 0);
+            return std::max(1, std::min(v, 4));
+        }();
+        const unsigned nb = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)device_sms() * occ,
+                                                                                  (n + SC_THREADS - 1) / SC_THREADS));
+        uint32_t cap = 1u << 14;
+        double tau = 0.0;
+        for (int attempt = 0; attempt < 16; ++attempt) {
+            uint32_t cap2 = 1;
+            while (cap2 < cap) cap2 <<= 1;
             Scratch S(st);
-            std::vector<uint32_t> hist;
-            std::vector<WPartial> parts;
-            int herr = 0;
-            run_wstats(w, n, st, S, hist, parts, herr);
-            if (herr & ERR_WEIGHT) return GIRG_EINVAL;
-            if (herr & ERR_WRANGE) return GIRG_ERANGE;
-            int emin = INT_MAX;
-            unsigned long long wb = 0;
-            for (const WPartial& q : parts)
-                if (q.e_b != INT_MAX) { emin = std::min(emin, q.e_b); wb = std::max(wb, q.wmax_bits); }
-            E.W = exact_W(parts, emin);
-            std::memcpy(&E.wmax, &wb, sizeof(double));
-        }
-        const double Ew = (beta - 1.0) / (beta - 2.0);
-        const double k0 = avg_deg * (1.0 - T) / (std::ldexp(1.0, d) * Ew);
-        auto set_tau = [&](double kappa) {
-            const double a = std::ldexp(kappa, d) / E.W;
-            E.tau = 0.25 / (a * E.wmax);
-            estimator_tail(w, n, E, st);
-        };
-        set_tau(k0);
-        auto f = [&](double kappa, double& out) -> bool {
-            for (int tries = 0; tries < 64; ++tries) {
-                if (E.f(kappa, out)) return true;
-                const double a = std::ldexp(kappa, d) / E.W;
-                if ((a * E.tau) * E.wmax <= 1.0) return false;  // non-finite value
-                set_tau(kappa);
+            char* blk = S.alloc<char>(Scratch::rounded(sizeof(ScaleCtl)) + Scratch::rounded(nb * sizeof(Acc192)) +
+                                      Scratch::rounded(nb * sizeof(TailSums)) + (size_t)(7 * cap2 + 8) * sizeof(double));
+            ScaleCtl* ctl = (ScaleCtl*)blk;
+            Acc192* wpart = (Acc192*)(blk + Scratch::rounded(sizeof(ScaleCtl)));
+            TailSums* tpart = (TailSums*)((char*)wpart + Scratch::rounded(nb * sizeof(Acc192)));
+            double* scr = (double*)((char*)tpart + Scratch::rounded(nb * sizeof(TailSums)));
+            ScaleCtl init;
+            std::memset(&init, 0, sizeof(init));
+            init.emin = INT_MAX;
+            GCHECK(cudaMemcpyAsync(ctl, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+            const double* wp = w;
+            uint32_t n32 = (uint32_t)n;
+            double avg = avg_deg, Tv = T, bv = beta, tv = tau;
+            int dv = d;
+            void* args[] = {(void*)&wp, &n32, &dv, &Tv, &avg, &bv, &tv, &wpart, &tpart, &scr, &cap2, &ctl};
+            GCHECK(cudaLaunchCooperativeKernel((const void*)k_scale, dim3(nb), dim3(SC_THREADS), args, 0, st));
+            ScaleCtl out;
+            GCHECK(cudaMemcpyAsync(&out, ctl, sizeof(out), cudaMemcpyDeviceToHost, st));
+            GCHECK(cudaStreamSynchronize(st));
+            if (out.err & ERR_WEIGHT) return GIRG_EINVAL;
+            if (out.err & ERR_WRANGE) return GIRG_ERANGE;
+            if (out.status == SC_OK) {
+                *kappa_out = out.kappa;
+                return GIRG_OK;
             }
-            return false;
-        };
-        double lo, hi, fv;
-        if (!f(k0, fv)) return GIRG_ERANGE;
-        int it = 0;
-        if (fv < avg_deg) {
-            lo = k0;
-            hi = 2.0 * k0;
-            for (;;) {
-                if (!f(hi, fv)) return GIRG_ERANGE;
-                if (!(fv < avg_deg)) break;
-                lo = hi;
-                hi *= 2.0;
-                if (++it > 2000) return GIRG_ERANGE;
+            if (out.status == SC_RANGE) return GIRG_ERANGE;
+            if (out.status == SC_CAP) {
+                cap = out.ncand + (out.ncand >> 3) + 64;
+                continue;
             }
-        } else {
-            hi = k0;
-            lo = 0.5 * k0;
-            for (;;) {
-                if (!f(lo, fv)) return GIRG_ERANGE;
-                if (fv < avg_deg) break;
-                hi = lo;
-                lo *= 0.5;
-                if (++it > 2000) return GIRG_ERANGE;
-            }
+            // SC_TAU: cover a wider kappa range around the failing kappa
+            tau = 1.0 / (64.0 * (std::ldexp(out.kappa, d) / out.W) * out.wmax);
         }
-        for (it = 0; it < 200 && hi / lo - 1.0 >= 1e-13; ++it) {
-            const double mid = std::sqrt(lo * hi);
-            if (!f(mid, fv)) return GIRG_ERANGE;
-            if (fv < avg_deg) lo = mid;
-            else hi = mid;
-        }
-        *kappa_out = 0.5 * (lo + hi);
-        return GIRG_OK;
+        return GIRG_ERANGE;
     } catch (const CudaFail& fl) {
         return map_cuda(fl.e);
     } catch (const std::bad_alloc&) {

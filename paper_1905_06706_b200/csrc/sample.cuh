@@ -1122,6 +1122,11 @@ struct TileSource {
                 const int lg = max(0, ((task >> 6) & 63) - Geo<D>::G);
                 t = make_task<D>(oi, task, ocode >> (D * (oI - lg)));
                 batch = 0;
+                // a task cell on or below the split level lies in one shard block: skip jobs whose
+                // children all belong to another shard before any setup work
+                if (lg >= a.sl && (a.nranks > 0 || a.blo > 0 || a.bhi < (1ull << (D * a.sl))) &&
+                    !owns<D>(a, t.Cpar << t.cs, t.l, t.i, t.j))
+                    continue;
             }
             const JobSetup js = setup_any<D, SCHEME>(a, S, t, batch);
             if (STATS && lane_id() == 0) C.ev2 += js.nseq2;
