@@ -1216,16 +1216,18 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
 // heavier candidates; host: the monotone search on f with E_R evaluated in O(|R|) over the
 // sorted candidates (same decomposition as DESIGN.md R12).
 // ======================================================================================
-// One cooperative launch (grid-wide barriers), one synchronisation for the caller:
+// Device part: ONE cooperative launch (grid-wide barriers) and one synchronisation:
 //   1  global e_min / w_max / input checks;  2  exact W (192-bit per-thread fixed point relative
 //   to e_min, block partials summed in 256 bits by block 0 and rounded once, R3);  3  kappa0,
-//   a0 = 2^d kappa0 / W and the tail threshold tau = 1/(64 a0 w_max): vertices with w <= tau are
-//   never saturated for kappa <= 64 kappa0, so their power sums (sum w, w^2, (w/wmax)^(1/T),
-//   (w/wmax)^(2/T)) are kappa-independent and summed once; heavier vertices are compacted;
-//   4  block 0 sorts the candidates (bitonic), forms suffix sums, and runs the exponential
-//   search + bisection on f with E_R in O(|R|) per evaluation (same decomposition as the
-//   oracle's or_f, R12).  The host re-launches only if the candidate buffer is too
-//   small or the search leaves the range covered by tau (status codes below).
+//   a0 = 2^d kappa0 / W and the tail threshold tau = 1/(2 a0 w_max): vertices with w <= tau are
+//   never saturated for kappa <= 2 kappa0, so their power sums (sum w, w^2, (w/wmax)^(1/T),
+//   (w/wmax)^(2/T)) are kappa-independent and summed once (fixed order: thread, warp, block,
+//   blocks in index order); heavier vertices are compacted.
+// Host part: the exponential search and bisection on f (same decomposition as the oracle's
+// or_f, R12) with E_R in O(|R|) over a LAZILY sorted prefix of the candidates (the
+// paper's App. B.2 device): each f(kappa) needs only R(kappa) = {w > 1/(a w_max)}
+// sorted; the unsorted rest enters through its sums.  A kappa outside the range covered by tau
+// re-launches the device pass with a smaller tau.
 constexpr int SC_THREADS = 256;
 struct Acc192 {
     unsigned long long v[3];
@@ -1234,14 +1236,14 @@ struct TailSums {
     double s1, s2, z1, z2;  // sum w, sum w^2, sum (w/wmax)^(1/T), sum (w/wmax)^(2/T) over w <= tau
 };
 struct ScaleCtl {
-    int emin;               // global minimum exponent (atomicMin)
-    int err;                // ERR_WEIGHT / ERR_WRANGE
+    int emin;  // global minimum exponent (atomicMin)
+    int err;   // ERR_WEIGHT / ERR_WRANGE
     unsigned long long wmax_bits;
-    unsigned int ncand;     // candidates (w > tau) seen
-    int status;             // 0 ok, 1 candidate buffer too small, 2 tau too large for a kappa, 3 range
-    double W, wmax, tau, kappa;
+    unsigned int ncand;  // candidates (w > tau) seen
+    int pad;
+    double W, wmax, tau, kappa0;
+    TailSums tail;
 };
-constexpr int SC_OK = 0, SC_CAP = 1, SC_TAU = 2, SC_RANGE = 3;
 
 __device__ __forceinline__ void add192(Acc192& a, unsigned long long lo, unsigned long long hi)
 {
@@ -1261,55 +1263,10 @@ __device__ __forceinline__ void add192(Acc192& a, const Acc192& b)
     a.v[2] += b.v[2];
 }
 
-// f(kappa) over the sorted candidates (decreasing) and the tail sums; false if kappa is outside
-// the range covered by tau (R must lie inside the candidates) or f is not finite
-struct DevEstimator {
-    uint64_t n;
-    int d;
-    double T, W, wmax, tau;
-    TailSums tail;
-    const double *cand, *zeta, *sc1, *sc2, *sz1, *sz2;
-    double *S1s, *SPs;
-    uint32_t nc;
-
-    __device__ bool f(double kappa, double& out) const
-    {
-        const double a = ldexp(kappa, d) / W;
-        if ((a * tau) * wmax > 1.0) return false;
-        const double invT = T > 0.0 ? 1.0 / T : 0.0;
-        const double G = T > 0.0 ? pow(sqrt(a) * wmax, invT) : 0.0;
-        uint32_t nr = 0;  // R = prefix of cand with (a w) wmax > 1
-        while (nr < nc && (a * cand[nr]) * wmax > 1.0) ++nr;
-        const double Wsmall = tail.s1 + sc1[nr], Zs = tail.z1 + sz1[nr], W2s = tail.s2 + sc2[nr],
-                     Z2s = tail.z2 + sz2[nr];
-        S1s[nr] = 0.0;
-        SPs[nr] = 0.0;
-        for (uint32_t k = nr; k-- > 0;) {
-            S1s[k] = S1s[k + 1] + cand[k];
-            SPs[k] = SPs[k + 1] + zeta[k];
-        }
-        const double Wt = Wsmall + S1s[0], Zt = Zs + SPs[0];
-        double Lsum = Wt * Wsmall - W2s;  // pairs (u outside R, any v != u): all non-E_R
-        double Psum = Zt * Zs - Z2s;      // in units of G^2
-        double nER = 0.0;
-        uint32_t m = nr;
-        for (uint32_t t = 0; t < nr; ++t) {
-            while (m > 0 && !((a * cand[t]) * cand[m - 1] > 1.0)) --m;
-            const bool self = t < m;
-            nER += (double)(m - (self ? 1 : 0));
-            Lsum += cand[t] * (Wsmall + S1s[m] - (self ? 0.0 : cand[t]));
-            Psum += zeta[t] * (Zs + SPs[m] - (self ? 0.0 : zeta[t]));
-        }
-        const double tot = T == 0.0 ? a * Lsum + nER : (a * Lsum - T * (G * G) * Psum) / (1.0 - T) + nER;
-        out = tot / (double)n;
-        return isfinite(out);
-    }
-};
-
 __global__ void __launch_bounds__(SC_THREADS) k_scale(const double* __restrict__ w, uint32_t n, int d, double T,
                                                       double avg_deg, double beta, double tau_in,
                                                       Acc192* __restrict__ wpart, TailSums* __restrict__ tpart,
-                                                      double* __restrict__ scr, uint32_t cap, ScaleCtl* ctl)
+                                                      double* __restrict__ cand, uint32_t cap, ScaleCtl* ctl)
 {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -1389,134 +1346,149 @@ __global__ void __launch_bounds__(SC_THREADS) k_scale(const double* __restrict__
         ctl->wmax = __longlong_as_double((long long)ctl->wmax_bits);
         const double Ew = (beta - 1.0) / (beta - 2.0);
         const double k0 = avg_deg * (1.0 - T) / (ldexp(1.0, d) * Ew);
-        ctl->kappa = k0;
+        ctl->kappa0 = k0;
         const double a0 = ldexp(k0, d) / ctl->W;
-        ctl->tau = tau_in > 0.0 ? tau_in : 1.0 / (64.0 * a0 * ctl->wmax);
+        ctl->tau = tau_in > 0.0 ? tau_in : 0.5 / (a0 * ctl->wmax);
         ctl->ncand = 0;
     }
     grid.sync();
     if (ctl->err) return;
     const double tau = ctl->tau, wmax = ctl->wmax, invT = T > 0.0 ? 1.0 / T : 0.0;
-    double* cand = scr;  // [cap2] candidates, then the sort / suffix arrays
-    // ---- 4: tail power sums (fixed-order per thread / warp / block) and candidates ----
-    {
-        double a1 = 0, a2 = 0, b1 = 0, b2 = 0;
-        for (size_t v = gtid; v < n; v += gstride) {
-            const double wv = w[v];
-            if (wv <= tau) {
-                a1 += wv;
-                a2 += wv * wv;
-                if (invT > 0.0) {
-                    const double z = pow(wv / wmax, invT);
-                    b1 += z;
-                    b2 += z * z;
-                }
-            } else {
-                const uint32_t k = atomicAdd(&ctl->ncand, 1u);
-                if (k < cap) cand[k] = wv;
+    // ---- 4: tail power sums and candidates ----
+    double a1 = 0, a2 = 0, b1 = 0, b2 = 0;
+    for (size_t v = gtid; v < n; v += gstride) {
+        const double wv = w[v];
+        if (wv <= tau) {
+            a1 += wv;
+            a2 += wv * wv;
+            if (invT > 0.0) {
+                const double z = pow(wv / wmax, invT);
+                b1 += z;
+                b2 += z * z;
             }
+        } else {
+            const uint32_t k = atomicAdd(&ctl->ncand, 1u);
+            if (k < cap) cand[k] = wv;
         }
-        for (int o = 16; o; o >>= 1) {
-            a1 += __shfl_down_sync(0xffffffffu, a1, o);
-            a2 += __shfl_down_sync(0xffffffffu, a2, o);
-            b1 += __shfl_down_sync(0xffffffffu, b1, o);
-            b2 += __shfl_down_sync(0xffffffffu, b2, o);
-        }
-        if (lane == 0) { sh_t[0][wid] = a1; sh_t[1][wid] = a2; sh_t[2][wid] = b1; sh_t[3][wid] = b2; }
-        __syncthreads();
-        if (tid == 0) {
-            TailSums t = {0, 0, 0, 0};
-            for (int k = 0; k < SC_THREADS / 32; ++k) { t.s1 += sh_t[0][k]; t.s2 += sh_t[1][k]; t.z1 += sh_t[2][k]; t.z2 += sh_t[3][k]; }
-            tpart[blockIdx.x] = t;
-        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        a1 += __shfl_down_sync(0xffffffffu, a1, o);
+        a2 += __shfl_down_sync(0xffffffffu, a2, o);
+        b1 += __shfl_down_sync(0xffffffffu, b1, o);
+        b2 += __shfl_down_sync(0xffffffffu, b2, o);
+    }
+    if (lane == 0) { sh_t[0][wid] = a1; sh_t[1][wid] = a2; sh_t[2][wid] = b1; sh_t[3][wid] = b2; }
+    __syncthreads();
+    if (tid == 0) {
+        TailSums t = {0, 0, 0, 0};
+        for (int k = 0; k < SC_THREADS / 32; ++k) { t.s1 += sh_t[0][k]; t.s2 += sh_t[1][k]; t.z1 += sh_t[2][k]; t.z2 += sh_t[3][k]; }
+        tpart[blockIdx.x] = t;
     }
     grid.sync();
-    if (blockIdx.x != 0) return;
-    // ---- 5: block 0: sort, suffix sums, search ----
-    const uint32_t nc = ctl->ncand;
-    if (nc > cap) {
-        if (tid == 0) ctl->status = SC_CAP;
-        return;
+    if (blockIdx.x == 0 && tid == 0) {  // fixed-order sum of the block partials
+        TailSums t = {0, 0, 0, 0};
+        for (unsigned b = 0; b < gridDim.x; ++b) { t.s1 += tpart[b].s1; t.s2 += tpart[b].s2; t.z1 += tpart[b].z1; t.z2 += tpart[b].z2; }
+        ctl->tail = t;
     }
-    uint32_t n2 = 1;
-    while (n2 < nc) n2 <<= 1;
-    for (uint32_t k = nc + tid; k < n2; k += SC_THREADS) cand[k] = -1.0;  // padding sorts last
-    __syncthreads();
-    for (uint32_t size = 2; size <= n2; size <<= 1)  // bitonic sort, decreasing
-        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            for (uint32_t i = tid; i < n2 / 2; i += SC_THREADS) {
-                const uint32_t lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-                const bool desc = (lo & size) == 0;
-                const double x = cand[lo], y = cand[hi];
-                if ((x < y) == desc) { cand[lo] = y; cand[hi] = x; }
-            }
-            __syncthreads();
-        }
-    double* zeta = cand + n2;
-    double* sc1 = zeta + n2;
-    double* sc2 = sc1 + n2 + 1;
-    double* sz1 = sc2 + n2 + 1;
-    double* sz2 = sz1 + n2 + 1;
-    double* S1s = sz2 + n2 + 1;
-    double* SPs = S1s + n2 + 1;
-    for (uint32_t k = tid; k < nc; k += SC_THREADS) zeta[k] = T > 0.0 ? pow(cand[k] / wmax, invT) : 0.0;
-    __syncthreads();
-    if (tid != 0) return;
-    sc1[nc] = sc2[nc] = sz1[nc] = sz2[nc] = 0.0;
-    for (uint32_t k = nc; k-- > 0;) {  // ascending weights: small terms first
-        sc1[k] = sc1[k + 1] + cand[k];
-        sc2[k] = sc2[k + 1] + cand[k] * cand[k];
-        sz1[k] = sz1[k + 1] + zeta[k];
-        sz2[k] = sz2[k + 1] + zeta[k] * zeta[k];
-    }
-    DevEstimator E;
-    E.n = n;
-    E.d = d;
-    E.T = T;
-    E.W = ctl->W;
-    E.wmax = wmax;
-    E.tau = tau;
-    E.tail = TailSums{0, 0, 0, 0};
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-        E.tail.s1 += tpart[b].s1; E.tail.s2 += tpart[b].s2; E.tail.z1 += tpart[b].z1; E.tail.z2 += tpart[b].z2;
-    }
-    E.cand = cand; E.zeta = zeta; E.sc1 = sc1; E.sc2 = sc2; E.sz1 = sz1; E.sz2 = sz2;
-    E.S1s = S1s; E.SPs = SPs; E.nc = nc;
-    double fv, lo, hi;
-    const double k0 = ctl->kappa;
-    auto fail_tau = [&](double kappa) { ctl->status = SC_TAU; ctl->kappa = kappa; };
-    if (!E.f(k0, fv)) { fail_tau(k0); return; }
-    int it = 0;
-    if (fv < avg_deg) {
-        lo = k0;
-        hi = 2.0 * k0;
-        for (;;) {
-            if (!E.f(hi, fv)) { fail_tau(hi); return; }
-            if (!(fv < avg_deg)) break;
-            lo = hi;
-            hi *= 2.0;
-            if (++it > 2000) { ctl->status = SC_RANGE; return; }
-        }
-    } else {
-        hi = k0;
-        lo = 0.5 * k0;
-        for (;;) {
-            if (!E.f(lo, fv)) { fail_tau(lo); return; }
-            if (fv < avg_deg) break;
-            hi = lo;
-            lo *= 0.5;
-            if (++it > 2000) { ctl->status = SC_RANGE; return; }
-        }
-    }
-    for (it = 0; it < 200 && hi / lo - 1.0 >= 1e-13; ++it) {
-        const double mid = sqrt(lo * hi);
-        if (!E.f(mid, fv)) { fail_tau(mid); return; }
-        if (fv < avg_deg) lo = mid;
-        else hi = mid;
-    }
-    ctl->kappa = 0.5 * (lo + hi);
-    ctl->status = SC_OK;
 }
+
+// host: f(kappa) over the candidates with a lazily sorted prefix
+struct LazyEstimator {
+    uint64_t n;
+    int d;
+    double T, W, wmax, tau;
+    TailSums tail;
+    std::vector<double> C;  // candidates: C[0, L) sorted decreasing, C[L, end) unsorted and < C[L-1]
+    size_t L = 0;
+    std::vector<double> zeta, suf1, suf2, sufz1, sufz2;  // over C[0, L): zeta and suffix sums (from k to L)
+    std::vector<double> pre1, prez;                      // prefix sums of C and zeta over C[0, L)
+    double r1 = 0, r2 = 0, rz1 = 0, rz2 = 0;             // sums over the unsorted rest
+    double rest_max = 0;                                 // largest unsorted candidate
+
+    double zf(double c) const { return T > 0.0 ? std::pow(c / wmax, 1.0 / T) : 0.0; }
+    void reset()
+    {
+        L = 0;
+        zeta.clear();
+        pre1.assign(1, 0.0);
+        prez.assign(1, 0.0);
+        suf1.assign(1, 0.0);
+        suf2.assign(1, 0.0);
+        sufz1.assign(1, 0.0);
+        sufz2.assign(1, 0.0);
+        rest_sums();
+    }
+    void rest_sums()
+    {
+        r1 = r2 = rz1 = rz2 = 0.0;
+        rest_max = 0.0;
+        for (size_t k = L; k < C.size(); ++k) {
+            const double z = zf(C[k]);
+            r1 += C[k];
+            r2 += C[k] * C[k];
+            rz1 += z;
+            rz2 += z * z;
+            rest_max = std::max(rest_max, C[k]);
+        }
+    }
+    // make C[0, L) hold every candidate > t, sorted decreasingly (the rest stays unsorted and
+    // below every sorted element, so a smaller t only appends)
+    void cover(double t)
+    {
+        if (L == C.size() || !(rest_max > t)) return;
+        auto mid = std::partition(C.begin() + L, C.end(), [t](double c) { return c > t; });
+        const size_t L2 = (size_t)(mid - C.begin());
+        std::sort(C.begin() + L, C.begin() + L2, [](double x, double y) { return x > y; });
+        L = L2;
+        zeta.resize(L);
+        for (size_t k = 0; k < L; ++k) zeta[k] = zf(C[k]);
+        suf1.assign(L + 1, 0.0);
+        suf2.assign(L + 1, 0.0);
+        sufz1.assign(L + 1, 0.0);
+        sufz2.assign(L + 1, 0.0);
+        for (size_t k = L; k-- > 0;) {  // ascending weights: small terms first
+            suf1[k] = suf1[k + 1] + C[k];
+            suf2[k] = suf2[k + 1] + C[k] * C[k];
+            sufz1[k] = sufz1[k + 1] + zeta[k];
+            sufz2[k] = sufz2[k + 1] + zeta[k] * zeta[k];
+        }
+        pre1.assign(L + 1, 0.0);
+        prez.assign(L + 1, 0.0);
+        for (size_t k = 0; k < L; ++k) {
+            pre1[k + 1] = pre1[k] + C[k];
+            prez[k + 1] = prez[k] + zeta[k];
+        }
+        rest_sums();
+    }
+    bool f(double kappa, double& out)
+    {
+        const double a = std::ldexp(kappa, d) / W;
+        if ((a * tau) * wmax > 1.0) return false;
+        const double invT = T > 0.0 ? 1.0 / T : 0.0;
+        const double G = T > 0.0 ? std::pow(std::sqrt(a) * wmax, invT) : 0.0;
+        cover(1.0 / (a * wmax));
+        size_t nr = 0;  // R = prefix of the sorted candidates with (a w) wmax > 1
+        while (nr < L && (a * C[nr]) * wmax > 1.0) ++nr;
+        const double Wsmall = tail.s1 + r1 + suf1[nr], Zs = tail.z1 + rz1 + sufz1[nr],
+                     W2s = tail.s2 + r2 + suf2[nr], Z2s = tail.z2 + rz2 + sufz2[nr];
+        // sums over R[m, nr) from the prefix sums of the sorted candidates
+        const double Wt = Wsmall + pre1[nr], Zt = Zs + prez[nr];
+        double Lsum = Wt * Wsmall - W2s;  // pairs (u outside R, any v != u): all non-E_R
+        double Psum = Zt * Zs - Z2s;      // in units of G^2
+        double nER = 0.0;
+        size_t m = nr;
+        for (size_t t = 0; t < nr; ++t) {
+            while (m > 0 && !((a * C[t]) * C[m - 1] > 1.0)) --m;
+            const bool self = t < m;
+            nER += (double)(m - (self ? 1 : 0));
+            Lsum += C[t] * (Wsmall + (pre1[nr] - pre1[m]) - (self ? 0.0 : C[t]));
+            Psum += zeta[t] * (Zs + (prez[nr] - prez[m]) - (self ? 0.0 : zeta[t]));
+        }
+        const double tot = T == 0.0 ? a * Lsum + nER : (a * Lsum - T * (G * G) * Psum) / (1.0 - T) + nER;
+        out = tot / (double)n;
+        return std::isfinite(out);
+    }
+};
 
 static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double T, double beta, double* kappa_out,
                       cudaStream_t st)
@@ -1532,44 +1504,124 @@ static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double
         }();
         const unsigned nb = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)device_sms() * occ,
                                                                                   (n + SC_THREADS - 1) / SC_THREADS));
-        uint32_t cap = 1u << 14;
+        uint32_t cap = (uint32_t)std::max<uint64_t>(1u << 16, n / 32);
         double tau = 0.0;
-        for (int attempt = 0; attempt < 16; ++attempt) {
-            uint32_t cap2 = 1;
-            while (cap2 < cap) cap2 <<= 1;
-            Scratch S(st);
-            char* blk = S.alloc<char>(Scratch::rounded(sizeof(ScaleCtl)) + Scratch::rounded(nb * sizeof(Acc192)) +
-                                      Scratch::rounded(nb * sizeof(TailSums)) + (size_t)(7 * cap2 + 8) * sizeof(double));
-            ScaleCtl* ctl = (ScaleCtl*)blk;
-            Acc192* wpart = (Acc192*)(blk + Scratch::rounded(sizeof(ScaleCtl)));
-            TailSums* tpart = (TailSums*)((char*)wpart + Scratch::rounded(nb * sizeof(Acc192)));
-            double* scr = (double*)((char*)tpart + Scratch::rounded(nb * sizeof(TailSums)));
-            ScaleCtl init;
-            std::memset(&init, 0, sizeof(init));
-            init.emin = INT_MAX;
-            GCHECK(cudaMemcpyAsync(ctl, &init, sizeof(init), cudaMemcpyHostToDevice, st));
-            const double* wp = w;
-            uint32_t n32 = (uint32_t)n;
-            double avg = avg_deg, Tv = T, bv = beta, tv = tau;
-            int dv = d;
-            void* args[] = {(void*)&wp, &n32, &dv, &Tv, &avg, &bv, &tv, &wpart, &tpart, &scr, &cap2, &ctl};
-            GCHECK(cudaLaunchCooperativeKernel((const void*)k_scale, dim3(nb), dim3(SC_THREADS), args, 0, st));
-            ScaleCtl out;
-            GCHECK(cudaMemcpyAsync(&out, ctl, sizeof(out), cudaMemcpyDeviceToHost, st));
-            GCHECK(cudaStreamSynchronize(st));
-            if (out.err & ERR_WEIGHT) return GIRG_EINVAL;
-            if (out.err & ERR_WRANGE) return GIRG_ERANGE;
-            if (out.status == SC_OK) {
-                *kappa_out = out.kappa;
-                return GIRG_OK;
+        LazyEstimator E;
+        E.n = n;
+        E.d = d;
+        E.T = T;
+        for (int attempt = 0; attempt < 24; ++attempt) {
+            // ---- device pass ----
+            {
+                Scratch S(st);
+                const size_t o1 = Scratch::rounded(sizeof(ScaleCtl)), o2 = o1 + Scratch::rounded(nb * sizeof(Acc192)),
+                             o3 = o2 + Scratch::rounded(nb * sizeof(TailSums));
+                char* blk = S.alloc<char>(o3 + (size_t)cap * sizeof(double));
+                ScaleCtl* ctl = (ScaleCtl*)blk;
+                Acc192* wpart = (Acc192*)(blk + o1);
+                TailSums* tpart = (TailSums*)(blk + o2);
+                double* cand = (double*)(blk + o3);
+                ScaleCtl init;
+                std::memset(&init, 0, sizeof(init));
+                init.emin = INT_MAX;
+                GCHECK(cudaMemcpyAsync(ctl, &init, sizeof(init), cudaMemcpyHostToDevice, st));
+                const double* wp = w;
+                uint32_t n32 = (uint32_t)n;
+                double avg = avg_deg, Tv = T, bv = beta, tv = tau;
+                int dv = d;
+                void* args[] = {(void*)&wp, &n32, &dv, &Tv, &avg, &bv, &tv, &wpart, &tpart, &cand, &cap, &ctl};
+                GCHECK(cudaLaunchCooperativeKernel((const void*)k_scale, dim3(nb), dim3(SC_THREADS), args, 0, st));
+                ScaleCtl out;
+                GCHECK(cudaMemcpyAsync(&out, ctl, sizeof(out), cudaMemcpyDeviceToHost, st));
+                GCHECK(cudaStreamSynchronize(st));
+                if (out.err & ERR_WEIGHT) return GIRG_EINVAL;
+                if (out.err & ERR_WRANGE) return GIRG_ERANGE;
+                if (out.ncand > cap) {  // candidate buffer too small: grow and repeat the pass
+                    cap = out.ncand + (out.ncand >> 3) + 64;
+                    tau = out.tau;
+                    continue;
+                }
+                E.W = out.W;
+                E.wmax = out.wmax;
+                E.tau = out.tau;
+                E.tail = out.tail;
+                E.C.resize(out.ncand);
+                if (out.ncand) {
+                    GCHECK(cudaMemcpyAsync(E.C.data(), cand, out.ncand * sizeof(double), cudaMemcpyDeviceToHost, st));
+                    GCHECK(cudaStreamSynchronize(st));
+                }
+                E.reset();
+                // ---- host search (exponential bracket, bisection in log kappa, R12) ----
+                const double k0 = out.kappa0;
+                double lo = 0, hi = 0, fv = 0, bad_kappa = 0;
+                bool ok = true;
+                auto F = [&](double kappa) {
+                    if (!ok) return false;
+                    if (!E.f(kappa, fv)) {
+                        const double a = std::ldexp(kappa, d) / E.W;
+                        if ((a * E.tau) * E.wmax > 1.0) bad_kappa = kappa;
+                        ok = false;
+                    }
+                    return ok;
+                };
+                int it = 0;
+                if (F(k0) && fv < avg_deg) {
+                    lo = k0;
+                    hi = 2.0 * k0;
+                    while (F(hi) && fv < avg_deg) {
+                        lo = hi;
+                        hi *= 2.0;
+                        if (++it > 2000) return GIRG_ERANGE;
+                    }
+                } else if (ok) {
+                    hi = k0;
+                    lo = 0.5 * k0;
+                    while (F(lo) && !(fv < avg_deg)) {
+                        hi = lo;
+                        lo *= 0.5;
+                        if (++it > 2000) return GIRG_ERANGE;
+                    }
+                }
+                // root of f(kappa) = avg_deg in [lo, hi] to a relative width of 1e-13 (R12): false
+                // position in log kappa with the Illinois rule, a bisection every third step
+                double glo = 0, ghi = 0;
+                if (ok && F(lo)) glo = fv - avg_deg;
+                if (ok && F(hi)) ghi = fv - avg_deg;
+                int side = 0;
+                for (it = 0; ok && it < 200 && hi / lo - 1.0 >= 1e-13; ++it) {
+                    double mid = std::sqrt(lo * hi);
+                    if (it % 3 != 2 && ghi > glo) {
+                        const double xl = std::log(lo), xh = std::log(hi);
+                        const double xm = xl - glo * (xh - xl) / (ghi - glo);
+                        const double cand = std::exp(xm);
+                        if (cand > lo && cand < hi) mid = cand;
+                    }
+                    if (!F(mid)) break;
+                    const double g = fv - avg_deg;
+                    if (g < 0) {
+                        lo = mid;
+                        glo = g;
+                        if (side == -1) ghi *= 0.5;
+                        side = -1;
+                    } else {
+                        hi = mid;
+                        ghi = g;
+                        if (side == 1) glo *= 0.5;
+                        side = 1;
+                    }
+                }
+                static const bool dbg = getenv("GIRG_SCALE_DEBUG") != nullptr;
+                if (dbg)
+                    fprintf(stderr, "[girg scale] attempt %d ncand %u sorted %zu tau %g ok %d iters %d kappa0 %g\n",
+                            attempt, out.ncand, E.L, E.tau, (int)ok, it, k0);
+                if (ok) {
+                    *kappa_out = 0.5 * (lo + hi);
+                    return GIRG_OK;
+                }
+                if (bad_kappa == 0) return GIRG_ERANGE;  // f not finite
+                // kappa beyond the range covered by tau: a smaller tau (up to 16x the failing kappa)
+                tau = 1.0 / (16.0 * (std::ldexp(bad_kappa, d) / E.W) * E.wmax);
             }
-            if (out.status == SC_RANGE) return GIRG_ERANGE;
-            if (out.status == SC_CAP) {
-                cap = out.ncand + (out.ncand >> 3) + 64;
-                continue;
-            }
-            // SC_TAU: cover a wider kappa range around the failing kappa
-            tau = 1.0 / (64.0 * (std::ldexp(out.kappa, d) / out.W) * out.wmax);
         }
         return GIRG_ERANGE;
     } catch (const CudaFail& fl) {
