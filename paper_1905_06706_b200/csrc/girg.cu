@@ -1104,6 +1104,7 @@ struct EdgeCall {
         a.bhi = hp.p.bhi;
         a.nranks = nranks;
         a.rank = rank;
+        a.sharded = nranks > 0 || blo > 0 || bhi < (1ull << (d * sl)) || sl * d >= 64;
         if (const char* e = getenv("GIRG_DEV_FLAGS")) a.dev_flags = (unsigned)atoi(e);
         PE.record(2, st);
         sample_and_fetch();

@@ -83,6 +83,7 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef GIRG_G2
 #define GIRG_G2 1
 #endif
+
 #ifndef GIRG_G1
 #define GIRG_G1 4
 #endif
@@ -192,6 +193,7 @@ struct SampleArgs {
     int sl;
     unsigned long long blo, bhi;
     uint32_t nranks, rank;  // interleaved ownership (nranks > 0), else the block range [blo, bhi)
+    int sharded;            // not the whole graph (ranked, or a block range other than everything)
 };
 
 struct TaskDesc {
@@ -433,6 +435,12 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
     const Plan* pl = a.pl;
     const unsigned lane = lane_id();
     const int nsub = 1 << t.cs;
+    // sharded runs: a task cell on or below the split level lies in one shard block, so a job of
+    // another shard is dropped before any setup work
+    if (a.sharded && t.lg >= a.sl && !owns<D>(a, t.Cpar << t.cs, t.l, t.i, t.j)) {
+        out.nchild = 0;
+        return 0;
+    }
     // the type-II bounds of the job (lanes 0, 1: classes 2, 3), loaded before the region so that
     // their latency overlaps the region loads
     te = t.t2 ? a.tab + (pl->tab_off[t.i * MAXL + t.j] + 2u * (uint32_t)(t.l - 2)) : nullptr;
@@ -505,7 +513,7 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
             if (e < nsub) {
                 ok = S.achild[e + 1] > S.achild[e];
                 const uint32_t A = (t.Cpar << t.cs) + (uint32_t)e;
-                ok = ok && owns<D>(a, A, t.l, t.i, t.j);
+ok = ok && owns<D>(a, A, t.l, t.i, t.j);
             }
             const unsigned bm = __ballot_sync(FULL, ok);
             const int rank = cnt + __popc(bm & ((1u << lane) - 1u));
@@ -1122,11 +1130,7 @@ struct TileSource {
                 const int lg = max(0, ((task >> 6) & 63) - Geo<D>::G);
                 t = make_task<D>(oi, task, ocode >> (D * (oI - lg)));
                 batch = 0;
-                // a task cell on or below the split level lies in one shard block: skip jobs whose
-                // children all belong to another shard before any setup work
-                if (lg >= a.sl && (a.nranks > 0 || a.blo > 0 || a.bhi < (1ull << (D * a.sl))) &&
-                    !owns<D>(a, t.Cpar << t.cs, t.l, t.i, t.j))
-                    continue;
+
             }
             const JobSetup js = setup_any<D, SCHEME>(a, S, t, batch);
             if (STATS && lane_id() == 0) C.ev2 += js.nseq2;
