@@ -178,8 +178,12 @@ int girg_edges_host(const double *w_host, const double *x_host, uint64_t n, int 
  *   cap          host array [B]
  *   m_out        host array [B]: the true edge count of each graph (also when > cap[g])
  *   status_out   host array [B] or NULL: the girg_status of each graph
- *   nstreams     concurrency: graphs run as independent pipelines on this many internal
- *                streams, one native host thread each (0 = default 8; clamped to [1, B])
+ *   nstreams     execution: for B >= 2 graphs of n <= 2^22 points (and B n < 2^31) the batch is
+ *                FUSED -- one launch per kernel for all graphs (weight statistics, one counting
+ *                sort over the concatenated cell spaces, sampling with one block row per graph)
+ *                and two synchronisations in total; nstreams < 0 (or larger graphs) runs the
+ *                graphs as independent girg_edges pipelines on |nstreams| internal streams, one
+ *                native host thread each (0 = 8)
  *   stream       ordering: the batch starts after the work already queued on `stream` and the
  *                call returns when every graph is done (it synchronises, as girg_edges does)
  * Returns GIRG_OK if every graph succeeded, else the status of the lowest failing index

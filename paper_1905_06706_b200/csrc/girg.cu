@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstddef>
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -23,6 +24,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <chrono>
 #include <memory>
 #include <thread>
 #include <mutex>
@@ -60,13 +62,20 @@ struct Plan {
     uint32_t lstart[MAXL + 1];  // first sorted position of layer i
     uint32_t cnt[MAXL];
     uint8_t I[MAXL];
-    uint8_t CL[MAXL * MAXL];
-    uint32_t tab_off[MAXL * MAXL];
     // task lists per (layer i, first level lf in 0..32): entries
-    // j | l<<6 | typeI<<12 | typeII<<13 in tasks[toff[i*33+lf] ...], tcnt[i*33+lf] entries
-    uint32_t toff[MAXL * 33];
+    // j | l<<6 | typeI<<12 | typeII<<13; layer i's tasks are stored once by decreasing task level
+    // at tasks[toff[i]], and the list of (i, lf) is their first tcnt[i*33+lf] entries
+    uint32_t toff[MAXL];
     uint16_t tcnt[MAXL * 33];
+    uint32_t tab_off[MAXL * MAXL];  // type-II bound table offset of the layer pair (i, j)
+    // ---- host only from here on (not uploaded) ----
+    uint8_t CL[MAXL * MAXL];
 };
+// bytes of a plan the device reads: everything up to the last used tab_off entry
+static inline size_t plan_upload_bytes(const Plan& p)
+{
+    return offsetof(Plan, tab_off) + (size_t)((p.L > 0 ? p.L - 1 : 0) * MAXL + p.L) * sizeof(uint32_t);
+}
 
 struct WPartial {
     unsigned long long lo, hi;  // sum of m * 2^(e - e_b) over the block
@@ -111,11 +120,20 @@ __device__ __forceinline__ void add128(unsigned long long& lo, unsigned long lon
     lo = t;
 }
 
-__global__ void __launch_bounds__(WS_THREADS) k_wstats(const double* __restrict__ w, uint32_t n,
+// Batched calls (girg_edges_batch) run B graphs in one launch: blockIdx.y is the graph, the
+// per-graph inputs come from the pointer array wb (nullptr: the single graph w), and the outputs
+// of graph g sit at hist + g HIST_BINS, part + g gridDim.x, err + g * err_stride.
+__global__ void __launch_bounds__(WS_THREADS) k_wstats(const double* __restrict__ w0, uint32_t n,
                                                        uint32_t* __restrict__ hist,
                                                        WPartial* __restrict__ part,
-                                                       int* __restrict__ err)
+                                                       int* __restrict__ err, const double* const* wb = nullptr,
+                                                       int err_stride = 0)
 {
+    const unsigned g = blockIdx.y;
+    const double* __restrict__ w = wb ? wb[g] : w0;
+    hist += (size_t)g * HIST_BINS;
+    part += (size_t)g * gridDim.x;
+    err += (size_t)g * err_stride;
     __shared__ uint32_t sh_hist[HIST_BINS];
     __shared__ int sh_emin, sh_emax;
     __shared__ unsigned long long sh_lo[WS_THREADS / 32], sh_hi[WS_THREADS / 32], sh_wmax;
@@ -196,10 +214,19 @@ __global__ void __launch_bounds__(WS_THREADS) k_wstats(const double* __restrict_
 // Morton index P:577-588) over the concatenated cell space; histogram of keys.
 // ======================================================================================
 template <int D>
-__global__ void k_keys(const double* __restrict__ w, const double* __restrict__ x, uint32_t n,
-                       const Plan* __restrict__ pl, uint32_t* __restrict__ key,
-                       uint32_t* __restrict__ cnt, int* __restrict__ err)
+__global__ void k_keys(const double* __restrict__ w0, const double* __restrict__ x0, uint32_t n,
+                       const Plan* __restrict__ pl0, uint32_t* __restrict__ key,
+                       uint32_t* __restrict__ cnt, int* __restrict__ err0, const double* const* wb = nullptr,
+                       const double* const* xb = nullptr, int err_stride = 0)
 {
+    // batched: graph g = blockIdx.y, its points at g n .. g n + n - 1 of the concatenated arrays,
+    // its plan's layer bases already offset into the concatenated cell space
+    const unsigned g = blockIdx.y;
+    const double* __restrict__ w = wb ? wb[g] : w0;
+    const double* __restrict__ x = xb ? xb[g] : x0;
+    const Plan* __restrict__ pl = pl0 + g;
+    int* err = err0 + (size_t)g * err_stride;
+    key += (size_t)g * n;
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     const unsigned long long bits = __double_as_longlong(w[v]);
@@ -337,7 +364,8 @@ __global__ void k_scatter(const uint32_t* __restrict__ key, uint32_t n, uint32_t
 constexpr uint32_t ORDER_SMALL = 32;
 __global__ void k_order(const uint2* __restrict__ tk, uint32_t n,
                         const uint32_t* __restrict__ P, uint32_t* __restrict__ sid, uint32_t* __restrict__ skey,
-                        uint32_t* __restrict__ inv, uint32_t* __restrict__ big, uint32_t* __restrict__ nbig)
+                        uint32_t* __restrict__ inv, uint32_t* __restrict__ big, uint32_t* __restrict__ nbig,
+                        uint32_t nper)
 {
     const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
@@ -358,7 +386,7 @@ __global__ void k_order(const uint2* __restrict__ tk, uint32_t n,
         for (uint32_t t = lo; t < hi; ++t) rank += tk[t].x < v;
         pos = lo + rank;
     }
-    sid[pos] = v;
+    sid[pos] = v % nper;  // the graph's own vertex id (batched calls: B graphs of nper points)
     skey[pos] = k;
     inv[v] = pos;
 }
@@ -372,7 +400,8 @@ __global__ void __launch_bounds__(OB_THREADS) k_order_big(const uint2* __restric
                                                          const uint32_t* __restrict__ big,
                                                          const uint32_t* __restrict__ nbig,
                                                          uint32_t* __restrict__ sid, uint32_t* __restrict__ skey,
-                                                         uint32_t* __restrict__ inv, uint32_t* __restrict__ tmp)
+                                                         uint32_t* __restrict__ inv, uint32_t* __restrict__ tmp,
+                                                         uint32_t nper)
 {
     __shared__ uint32_t base[256];
     __shared__ uint32_t wcnt[OB_WARPS][256];
@@ -434,7 +463,7 @@ __global__ void __launch_bounds__(OB_THREADS) k_order_big(const uint2* __restric
         const uint32_t* fin = (passes & 1) ? sid : tmp;
         for (uint32_t t = tid; t < c; t += OB_THREADS) {
             const uint32_t v = fin[lo + t];
-            if (fin != sid) sid[lo + t] = v;
+            sid[lo + t] = v % nper;
             skey[lo + t] = key;
             inv[v] = lo + t;
         }
@@ -445,9 +474,14 @@ __global__ void __launch_bounds__(OB_THREADS) k_order_big(const uint2* __restric
 // sorted point records rec[pos] = (x_0, .., x_{d-1}, w): coalesced reads in vertex order,
 // one aligned 16/32/48-byte record write per vertex
 template <int D>
-__global__ void k_place(const uint32_t* __restrict__ inv, uint32_t n, const double* __restrict__ w,
-                        const double* __restrict__ x, double* __restrict__ rec)
+__global__ void k_place(const uint32_t* __restrict__ inv, uint32_t n, const double* __restrict__ w0,
+                        const double* __restrict__ x0, double* __restrict__ rec, const double* const* wb = nullptr,
+                        const double* const* xb = nullptr)
 {
+    const unsigned g = blockIdx.y;  // batched: graph g's points are entries g n .. g n + n - 1 of inv
+    const double* __restrict__ w = wb ? wb[g] : w0;
+    const double* __restrict__ x = xb ? xb[g] : x0;
+    inv += (size_t)g * n;
     const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     constexpr int RW = Geo<D>::RECW;
@@ -757,27 +791,38 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
     // point of Cg: the one point of Cg whose first level lf (the coarsest level on which it is the
     // first point of its cell; it stays first on every finer level) is <= lg.  Type-I if
     // l == CL(i,j), type-II if 2 <= l (T > 0).
+    // The list of (layer i, lf) is every task of layer i with lg >= lf: layer i's tasks are stored
+    // once, by decreasing lg, and each list is a prefix of them (the order of the tasks in a list
+    // only schedules the work; the edge set does not depend on it).
     hp.tasks.clear();
     const int G = d == 1 ? GIRG_G1 : (d == 2 ? GIRG_G2 : 1);  // Geo<D>::G
-    for (int i = 0; i < p.L; ++i)
-        for (int lf = 0; lf <= 32; ++lf) {
-            p.toff[i * 33 + lf] = (uint32_t)hp.tasks.size();
-            uint32_t c = 0;
-            if (p.cnt[i] && lf <= p.I[i])
-                for (int j = i; j < p.L; ++j) {
-                    if (!p.cnt[j]) continue;
-                    const int cl = p.CL[i * MAXL + j];
-                    for (int l = 0; l <= cl; ++l) {
-                        const int lg = std::max(0, l - G);
-                        const int t1 = l == cl, t2 = T > 0.0 && l >= 2;
-                        if (lg < lf || (!t1 && !t2)) continue;
-                        hp.tasks.push_back((uint16_t)(j | (l << 6) | (t1 << 12) | (t2 << 13)));
-                        ++c;
-                    }
+    std::vector<std::pair<int, uint16_t>> E;                  // (lg, task) of layer i
+    for (int i = 0; i < p.L; ++i) {
+        E.clear();
+        if (p.cnt[i])
+            for (int j = i; j < p.L; ++j) {
+                if (!p.cnt[j]) continue;
+                const int cl = p.CL[i * MAXL + j];
+                for (int l = 0; l <= cl; ++l) {
+                    const int lg = std::max(0, l - G);
+                    const int t1 = l == cl, t2 = T > 0.0 && l >= 2;
+                    if (!t1 && !t2) continue;
+                    E.emplace_back(lg, (uint16_t)(j | (l << 6) | (t1 << 12) | (t2 << 13)));
                 }
-            if (c > 0xFFFF) return GIRG_ERANGE;
-            p.tcnt[i * 33 + lf] = (uint16_t)c;
+            }
+        std::stable_sort(E.begin(), E.end(), [](const std::pair<int, uint16_t>& x, const std::pair<int, uint16_t>& y) {
+            return x.first > y.first;
+        });
+        const uint32_t off = (uint32_t)hp.tasks.size();
+        p.toff[i] = off;
+        for (const auto& e : E) hp.tasks.push_back(e.second);
+        if (E.size() > 0xFFFF) return GIRG_ERANGE;
+        size_t c = E.size();
+        for (int lf = 0; lf <= 32; ++lf) {
+            while (c > 0 && E[c - 1].first < lf) --c;
+            p.tcnt[i * 33 + lf] = (uint16_t)((p.cnt[i] && lf <= p.I[i]) ? c : 0);
         }
+    }
     if (hp.tasks.empty()) hp.tasks.push_back(0);
     return GIRG_OK;
 }
@@ -819,12 +864,12 @@ static void launch_index(const double* w, const double* x, uint32_t n, const Pla
     k_scan_top<<<1, 1024, 0, st>>>(bsum, nb);
     k_scan_final<<<nb, SCAN_THREADS, 0, st>>>(cnt, len, bsum, P);
     k_scatter<<<grid_for(n, 256), 256, 0, st>>>(key, n, cnt, tk);
-    k_order<<<grid_for(n, 256), 256, 0, st>>>(tk, n, P, sid, skey, inv, big, nbig);
+    k_order<<<grid_for(n, 256), 256, 0, st>>>(tk, n, P, sid, skey, inv, big, nbig, n);
     {
         int bits = 1;
         while (bits < 32 && (1ull << bits) < (unsigned long long)n) ++bits;
         const unsigned gb = (unsigned)std::min<uint64_t>((uint64_t)device_sms() * 4u, n / (ORDER_SMALL + 1) + 1);
-        k_order_big<<<gb, OB_THREADS, 0, st>>>(tk, (bits + 7) / 8, big, nbig, sid, skey, inv, key);
+        k_order_big<<<gb, OB_THREADS, 0, st>>>(tk, (bits + 7) / 8, big, nbig, sid, skey, inv, key, n);
     }
     k_place<D><<<grid_for(n, 256), 256, 0, st>>>(inv, n, w, x, rec);
     GCHECK(cudaGetLastError());
@@ -1046,12 +1091,12 @@ struct EdgeCall {
         char* stage = PE.staging(up_bytes + 256);
         hmisc = stage ? stage + up_bytes : hmisc_local;
         if (stage) {
-            std::memcpy(stage, &hp.p, sizeof(Plan));
+            std::memcpy(stage, &hp.p, plan_upload_bytes(hp.p));
             std::memcpy(stage + up_plan, hp.tab.data(), hp.tab.size() * sizeof(TabEntry));
             std::memcpy(stage + up_plan + up_tab, hp.tasks.data(), hp.tasks.size() * sizeof(uint16_t));
             GCHECK(cudaMemcpyAsync(d_up, stage, up_bytes, cudaMemcpyHostToDevice, st));
         } else {
-            GCHECK(cudaMemcpyAsync(d_plan, &hp.p, sizeof(Plan), cudaMemcpyHostToDevice, st));
+            GCHECK(cudaMemcpyAsync(d_plan, &hp.p, plan_upload_bytes(hp.p), cudaMemcpyHostToDevice, st));
             GCHECK(cudaMemcpyAsync(d_tab, hp.tab.data(), hp.tab.size() * sizeof(TabEntry), cudaMemcpyHostToDevice, st));
             GCHECK(cudaMemcpyAsync(d_tasks, hp.tasks.data(), hp.tasks.size() * sizeof(uint16_t),
                                    cudaMemcpyHostToDevice, st));
@@ -1105,6 +1150,7 @@ struct EdgeCall {
         a.nranks = nranks;
         a.rank = rank;
         a.sharded = nranks > 0 || blo > 0 || bhi < (1ull << (d * sl)) || sl * d >= 64;
+        a.p0 = 0;
         if (const char* e = getenv("GIRG_DEV_FLAGS")) a.dev_flags = (unsigned)atoi(e);
         PE.record(2, st);
         sample_and_fetch();
@@ -1733,6 +1779,264 @@ extern "C" int girg_edges_host(const double* w_host, const double* x_host, uint6
     }
 }
 
+// Fused batch: B graphs of n points as ONE problem.  One launch
+// computes every graph's weight statistics (blockIdx.y = graph); after the single read-back the
+// host makes the B plans and offsets each graph's cell space into one concatenated key space, so
+// that ONE counting sort (keys, scan, scatter, in-cell order, records) builds every graph's
+// Lemma-1 index at once (graph g's sorted points are entries g n .. g n + n - 1, its vertex ids
+// local); the sampling kernels run all graphs in one launch each (blockIdx.y = graph, per-graph
+// arguments in device memory).  Two host synchronisations for the whole batch.  Graph g's edge
+// set is exactly its girg_edges result: the plan, index and keyed draws are the same.
+template <int D>
+static int batch_fused(int B, const double* const* w_dev, const double* const* x_dev, uint64_t n, double T,
+                       const double* kappa, const uint64_t* seed, uint32_t* const* edges_dev, const uint64_t* cap,
+                       uint64_t* m_out, int* status, cudaStream_t st)
+{
+    constexpr int d = D;
+    const uint32_t n32 = (uint32_t)n;
+    const uint64_t N = (uint64_t)B * n;
+    static const bool dbg = getenv("GIRG_BATCH_DEBUG") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto t0 = now();
+    auto lap = [&](const char* what) {
+        if (!dbg) return;
+        const auto t = now();
+        fprintf(stderr, "[girg batch] %-28s %8.1f us\n", what, std::chrono::duration<double, std::micro>(t - t0).count());
+        t0 = t;
+    };
+    PhaseEvents PE;
+    Scratch S(st);
+    // ---- weight statistics of every graph (one launch, one read-back) ----
+    const unsigned tiles = grid_for(n, WS_TILE);
+    const size_t o_err = (size_t)B * HIST_BINS * 4, o_part = Scratch::rounded(o_err + (size_t)B * 16),
+                 wst_bytes = o_part + (size_t)B * tiles * sizeof(WPartial);
+    char* wst = S.alloc<char>(wst_bytes);
+    const double** d_ptr = (const double**)S.alloc<char>(2 * (size_t)B * sizeof(void*));
+    {
+        std::vector<const double*> hp(2 * (size_t)B);
+        for (int g = 0; g < B; ++g) {
+            hp[g] = w_dev[g];
+            hp[B + g] = x_dev[g];
+        }
+        GCHECK(cudaMemcpyAsync(d_ptr, hp.data(), hp.size() * sizeof(void*), cudaMemcpyHostToDevice, st));
+        GCHECK(cudaStreamSynchronize(st));  // pageable source
+    }
+    const double* const* d_w = d_ptr;
+    const double* const* d_x = d_ptr + B;
+    GCHECK(cudaMemsetAsync(wst, 0, o_part, st));
+    k_wstats<<<dim3(tiles, B), WS_THREADS, 0, st>>>(nullptr, n32, (uint32_t*)wst, (WPartial*)(wst + o_part),
+                                                    (int*)(wst + o_err), d_w, 4);
+    GCHECK(cudaGetLastError());
+    char* hw = PE.staging(std::max<size_t>(wst_bytes, 1 << 20));
+    std::vector<char> hw_pageable;
+    if (!hw) {
+        hw_pageable.resize(wst_bytes);
+        hw = hw_pageable.data();
+    }
+    GCHECK(cudaMemcpyAsync(hw, wst, wst_bytes, cudaMemcpyDeviceToHost, st));
+    GCHECK(cudaStreamSynchronize(st));
+    lap("weight statistics + sync");
+    // ---- plans (host threads for large batches), concatenated cell space ----
+    // the plans live in a per-thread cache: a fresh 2 MB of HostPlans per call costs more in page
+    // faults than making the plans
+    static thread_local std::vector<HostPlan> hp_cache;
+    if (hp_cache.size() < (size_t)B) hp_cache.resize(B);
+    HostPlan* hp = hp_cache.data();
+    std::vector<int> prc(B, GIRG_OK);
+    auto plan_one = [&](int g) {
+        const int herr = ((const int*)(hw + o_err))[4 * g];
+        if (herr & ERR_WEIGHT) { prc[g] = GIRG_EINVAL; return; }
+        if (herr & ERR_WRANGE) { prc[g] = GIRG_ERANGE; return; }
+        std::vector<uint32_t> hist((const uint32_t*)hw + (size_t)g * HIST_BINS,
+                                   (const uint32_t*)hw + (size_t)(g + 1) * HIST_BINS);
+        std::vector<WPartial> parts((const WPartial*)(hw + o_part) + (size_t)g * tiles,
+                                    (const WPartial*)(hw + o_part) + (size_t)(g + 1) * tiles);
+        prc[g] = make_plan(hist, parts, n, d, T, kappa[g], hp[g]);
+        hp[g].p.sl = 0;
+        hp[g].p.blo = 0;
+        hp[g].p.bhi = 1;
+    };
+    {
+        static const int nth_env = getenv("GIRG_BATCH_PLAN_THREADS") ? atoi(getenv("GIRG_BATCH_PLAN_THREADS")) : 0;
+        const int nth = nth_env > 0 ? nth_env : (B >= 16 ? std::min(8, B / 8) : 1);
+        std::atomic<int> next{0};
+        auto work = [&]() {
+            for (int g; (g = next.fetch_add(1)) < B;) plan_one(g);
+        };
+        std::vector<std::thread> pool;
+        for (int k = 1; k < nth; ++k) pool.emplace_back(work);
+        work();
+        for (std::thread& t : pool) t.join();
+    }
+    lap("plans");
+    for (int g = 0; g < B; ++g)
+        if (prc[g] != GIRG_OK) return 1;  // the caller runs the per-graph path, which reports it
+    std::vector<uint64_t> gbase(B + 1, 0);
+    for (int g = 0; g < B; ++g) gbase[g + 1] = gbase[g] + hp[g].K;
+    const uint64_t K = gbase[B];
+    if (K + 1 >= 0xFFFFFFFFull) return 1;
+    size_t ntab = 0, ntask = 0;
+    std::vector<size_t> tab_off(B), task_off(B);
+    for (int g = 0; g < B; ++g) {
+        Plan& p = hp[g].p;
+        for (int i = 0; i <= p.L; ++i) p.base[i] += (uint32_t)gbase[g];
+        tab_off[g] = ntab;
+        task_off[g] = ntask;
+        ntab += hp[g].tab.size();
+        ntask += hp[g].tasks.size();
+    }
+    // ---- scratch ----
+    const int recw = Geo<D>::RECW;
+    const unsigned items_cap = std::max<unsigned>(4096u, n32 / 2);
+    const size_t up_plan = Scratch::rounded((size_t)B * sizeof(Plan)), up_tab = Scratch::rounded(ntab * sizeof(TabEntry)),
+                 up_task = Scratch::rounded(ntask * sizeof(uint16_t)), up_args = Scratch::rounded((size_t)B * sizeof(SampleArgs)),
+                 up_bytes = up_plan + up_tab + up_task + up_args;
+    S.reserve(Scratch::rounded(up_bytes) + Scratch::rounded((size_t)B * 256) + Scratch::rounded(16) +
+              6 * Scratch::rounded(N * 4) + 2 * Scratch::rounded((K + 1) * 4) +
+              Scratch::rounded((grid_for(K + 1, SCAN_TILE) + 1) * 4) + Scratch::rounded((size_t)recw * N * 8) +
+              Scratch::rounded((size_t)B * items_cap * sizeof(BigItem)) + Scratch::rounded((2 * (N / (ORDER_SMALL + 1) + 1)) * 4));
+    char* d_up = S.alloc<char>(up_bytes);
+    Plan* d_plan = (Plan*)d_up;
+    TabEntry* d_tab = (TabEntry*)(d_up + up_plan);
+    uint16_t* d_tasks = (uint16_t*)(d_up + up_plan + up_tab);
+    SampleArgs* d_args = (SampleArgs*)(d_up + up_plan + up_tab + up_task);
+    char* misc = S.alloc<char>((size_t)B * 256);
+    uint32_t* nbig = S.alloc<uint32_t>(4);
+    uint32_t* key = S.alloc<uint32_t>(N);
+    uint2* tk = S.alloc<uint2>(N);
+    uint32_t* inv = S.alloc<uint32_t>(N);
+    uint32_t* cnt = S.alloc<uint32_t>(K + 1);
+    uint32_t* P = S.alloc<uint32_t>(K + 1);
+    uint32_t* bsum = S.alloc<uint32_t>(grid_for(K + 1, SCAN_TILE) + 1);
+    uint32_t* sid = S.alloc<uint32_t>(N);
+    uint32_t* skey = S.alloc<uint32_t>(N);
+    double* rec = S.alloc<double>((size_t)recw * N);
+    BigItem* items = S.alloc<BigItem>((size_t)B * items_cap);
+    uint32_t* big = S.alloc<uint32_t>(2 * (N / (ORDER_SMALL + 1) + 1));
+    // ---- per-graph sampler arguments, written straight into page-locked staging, one upload ----
+    char* stage = PE.staging(up_bytes + (size_t)B * 256);
+    std::vector<char> up_pageable;
+    char* up = stage;
+    if (!up) {
+        up_pageable.resize(up_bytes + (size_t)B * 256);
+        up = up_pageable.data();
+    }
+    char* hmisc = up + up_bytes;
+    for (int g = 0; g < B; ++g) {
+        std::memcpy(up + (size_t)g * sizeof(Plan), &hp[g].p, plan_upload_bytes(hp[g].p));
+        std::memcpy(up + up_plan + tab_off[g] * sizeof(TabEntry), hp[g].tab.data(), hp[g].tab.size() * sizeof(TabEntry));
+        std::memcpy(up + up_plan + up_tab + task_off[g] * sizeof(uint16_t), hp[g].tasks.data(),
+                    hp[g].tasks.size() * sizeof(uint16_t));
+        SampleArgs a;
+        std::memset(&a, 0, sizeof(a));
+        char* mg = misc + (size_t)g * 256;
+        a.pl = d_plan + g;
+        a.tab = d_tab + tab_off[g];
+        a.tasks = d_tasks + task_off[g];
+        a.skey = skey + (size_t)g * n;
+        a.rec = rec + (size_t)g * n * recw;
+        a.sid = sid + (size_t)g * n;
+        a.P = P;
+        a.n = n32;
+        a.ntiles = (n32 + 31) / 32;
+        a.k0 = (uint32_t)seed[g];
+        a.k1 = (uint32_t)(seed[g] >> 32);
+        a.edges = (uint2*)edges_dev[g];
+        a.cap = cap[g];
+        a.m = (unsigned long long*)(mg + 16);
+        a.tile_ctr = (unsigned int*)(mg + 24);
+        a.nitems = (unsigned int*)(mg + 28);
+        a.item_ctr = (unsigned int*)(mg + 128);
+        a.stats = nullptr;
+        a.err = (int*)mg;
+        a.items = items + (size_t)g * items_cap;
+        a.items_cap = items_cap;
+        a.nP = K + 1;
+        a.ntab = (unsigned)hp[g].tab.size();
+        a.ntasks = (unsigned)hp[g].tasks.size();
+        a.big_work = big_work(d, n);
+        a.item_work = item_work(d, n);
+        a.T = hp[g].p.T;
+        a.s = hp[g].p.s;
+        a.invT = hp[g].p.invT;
+        a.sl = 0;
+        a.blo = 0;
+        a.bhi = 1;
+        a.nranks = 0;
+        a.rank = 0;
+        a.sharded = 0;
+        a.p0 = (uint32_t)((uint64_t)g * n);
+        std::memcpy(up + up_plan + up_tab + up_task + (size_t)g * sizeof(SampleArgs), &a, sizeof(a));
+    }
+    GCHECK(cudaMemcpyAsync(d_up, up, up_bytes, cudaMemcpyHostToDevice, st));
+    if (!stage) GCHECK(cudaStreamSynchronize(st));  // pageable source must outlive the copy
+    lap("scratch + args + upload");
+    GCHECK(cudaMemsetAsync(misc, 0, (size_t)B * 256, st));
+    GCHECK(cudaMemsetAsync(nbig, 0, 16, st));
+    // ---- one index build over the concatenated problem ----
+    GCHECK(cudaMemsetAsync(cnt, 0, (K + 1) * sizeof(uint32_t), st));
+    k_keys<D><<<dim3(grid_for(n, 256), B), 256, 0, st>>>(nullptr, nullptr, n32, d_plan, key, cnt, (int*)misc, d_w,
+                                                         d_x, 64);
+    const unsigned nbs = grid_for(K + 1, SCAN_TILE);
+    k_scan_reduce<<<nbs, SCAN_THREADS, 0, st>>>(cnt, K + 1, bsum);
+    k_scan_top<<<1, 1024, 0, st>>>(bsum, nbs);
+    k_scan_final<<<nbs, SCAN_THREADS, 0, st>>>(cnt, K + 1, bsum, P);
+    k_scatter<<<grid_for(N, 256), 256, 0, st>>>(key, (uint32_t)N, cnt, tk);
+    k_order<<<grid_for(N, 256), 256, 0, st>>>(tk, (uint32_t)N, P, sid, skey, inv, big, nbig, n32);
+    {
+        int bits = 1;
+        while (bits < 32 && (1ull << bits) < N) ++bits;
+        const unsigned gb = (unsigned)std::min<uint64_t>((uint64_t)device_sms() * 4u, N / (ORDER_SMALL + 1) + 1);
+        k_order_big<<<gb, OB_THREADS, 0, st>>>(tk, (bits + 7) / 8, big, nbig, sid, skey, inv, key, n32);
+    }
+    k_place<D><<<dim3(grid_for(n, 256), B), 256, 0, st>>>(inv, n32, nullptr, nullptr, rec, d_w, d_x);
+    GCHECK(cudaGetLastError());
+    // ---- sampling, every graph in one launch per kernel ----
+    {
+        constexpr int WPB = Geo<D>::WPB, TPB = 32 * WPB;
+        const size_t smem = sizeof(WarpSmem<D>) * WPB;
+        smem_optin(k_sample_b<D, SCHEME_MERGED, false>, smem);
+        smem_optin(k_big_b<D, SCHEME_MERGED, false>, smem);
+        static const int occ = [] {
+            int v = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_sample_b<D, SCHEME_MERGED, false>, TPB,
+                                                          sizeof(WarpSmem<D>) * WPB);
+            return std::max(v, 1);
+        }();
+        const unsigned wtiles = ((n32 + 31) / 32 + WPB - 1) / WPB;
+        const unsigned per = std::max(1u, std::min<unsigned>(wtiles, (unsigned)((2ull * device_sms() * occ + B - 1) / B)));
+        k_sample_b<D, SCHEME_MERGED, false><<<dim3(per, B), TPB, smem, st>>>(d_args);
+        k_big_b<D, SCHEME_MERGED, false><<<dim3(per, B), TPB, smem, st>>>(d_args);
+        GCHECK(cudaGetLastError());
+    }
+    lap("launches");
+    GCHECK(cudaMemcpyAsync(hmisc, misc, (size_t)B * 256, cudaMemcpyDeviceToHost, st));
+    GCHECK(cudaStreamSynchronize(st));
+    lap("index + sampling + sync");
+    for (int g = 0; g < B; ++g) {
+        const char* mg = hmisc + (size_t)g * 256;
+        int derr;
+        unsigned long long m;
+        std::memcpy(&derr, mg, sizeof(int));
+        std::memcpy(&m, mg + 16, sizeof(m));
+        if (derr & ERR_POS) {
+            status[g] = GIRG_EINVAL;
+            m_out[g] = 0;
+            continue;
+        }
+        if (derr & ERR_ITEMS) {  // item queue overflow (rare for small graphs): this graph alone
+            uint64_t mm = 0;
+            status[g] = edges_impl(w_dev[g], x_dev[g], n, d, T, kappa[g], seed[g], 0, 0, 1, SCHEME_MERGED,
+                                   edges_dev[g], cap[g], &mm, nullptr, st);
+            m_out[g] = mm;
+            continue;
+        }
+        m_out[g] = m;
+        status[g] = m > cap[g] ? GIRG_ECAPACITY : GIRG_OK;
+    }
+    return 0;
+}
+
 // Batched small graphs: each graph is one unchanged girg_edges pipeline
 // (EdgeCall: two host waits, for the weight statistics the plan needs and for the edge count).
 // A pool of native host threads, each with its own stream, runs them concurrently, so one
@@ -1749,8 +2053,36 @@ extern "C" int girg_edges_batch(int B, const double* const* w_dev, const double*
         if (EdgeCall::validate(w_dev[g], x_dev[g], n, d, T, kappa[g], 0, 0, 1, SCHEME_MERGED, edges_dev[g], cap[g],
                                m_out + g) != GIRG_OK)
             return GIRG_EINVAL;
-    const int nt = std::max(1, std::min(B, nstreams > 0 ? nstreams : 8));
     cudaStream_t st = (cudaStream_t)stream;
+    if (B >= 2 && nstreams >= 0 && n <= (1ull << 22) && (uint64_t)B * n < (1ull << 31)) {  // fused batch
+        std::vector<int> status(B, GIRG_OK);
+        int used = 1;
+        try {
+            switch (d) {
+                case 1: used = batch_fused<1>(B, w_dev, x_dev, n, T, kappa, seed, edges_dev, cap, m_out, status.data(), st); break;
+                case 2: used = batch_fused<2>(B, w_dev, x_dev, n, T, kappa, seed, edges_dev, cap, m_out, status.data(), st); break;
+                case 3: used = batch_fused<3>(B, w_dev, x_dev, n, T, kappa, seed, edges_dev, cap, m_out, status.data(), st); break;
+                case 4: used = batch_fused<4>(B, w_dev, x_dev, n, T, kappa, seed, edges_dev, cap, m_out, status.data(), st); break;
+                default: used = batch_fused<5>(B, w_dev, x_dev, n, T, kappa, seed, edges_dev, cap, m_out, status.data(), st); break;
+            }
+        } catch (const CudaFail& f) {
+            return map_cuda(f.e);
+        } catch (const std::bad_alloc&) {
+            return GIRG_ENOMEM;
+        } catch (...) {
+            g_last_cuda = "internal error: unexpected exception";
+            return GIRG_ECUDA;
+        }
+        if (used == 0) {
+            int rc = GIRG_OK;
+            for (int g = 0; g < B; ++g) {
+                if (status_out) status_out[g] = status[g];
+                if (rc == GIRG_OK && status[g] != GIRG_OK) rc = status[g];
+            }
+            return rc;
+        }
+    }
+    const int nt = std::max(1, std::min(B, nstreams > 0 ? nstreams : (nstreams < 0 ? -nstreams : 8)));
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return map_cuda(cudaGetLastError());
     std::vector<cudaStream_t> ss(nt, nullptr);

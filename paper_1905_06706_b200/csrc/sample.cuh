@@ -194,6 +194,7 @@ struct SampleArgs {
     unsigned long long blo, bhi;
     uint32_t nranks, rank;  // interleaved ownership (nranks > 0), else the block range [blo, bhi)
     int sharded;            // not the whole graph (ranked, or a block range other than everything)
+    uint32_t p0;            // batched calls: first sorted position of this graph in the shared index
 };
 
 struct TaskDesc {
@@ -494,12 +495,12 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
                 const int q = per == PER1 ? e / PER1 : e / per, k = e - q * per;
                 const unsigned long long cell = ((unsigned long long)S.par[q] << t.cs) + (unsigned)k;
                 GCHK(bj + (cell << shj) < a.nP);
-                S.rstart[q][k] = __ldg(&a.P[bj + (cell << shj)]);
+                S.rstart[q][k] = __ldg(&a.P[bj + (cell << shj)]) - a.p0;
             } else {
                 const int k = e - t.npar * per;
                 const unsigned long long cell = ((unsigned long long)t.Cpar << t.cs) + (unsigned)k;
                 GCHK(bi + (cell << shi) < a.nP);
-                S.achild[k] = __ldg(&a.P[bi + (cell << shi)]);
+                S.achild[k] = __ldg(&a.P[bi + (cell << shi)]) - a.p0;
             }
         }
     }
@@ -1082,7 +1083,7 @@ struct TileSource {
             }
         }
         cnt = lf == 255 ? 0u : pl->tcnt[i * 33 + lf];
-        toffv = lf == 255 ? 0u : pl->toff[i * 33 + lf];
+        toffv = lf == 255 ? 0u : pl->toff[i];
         Ii = pl->I[i];
         start = warp_excl_scan(cnt, total);
         tk = 0;
@@ -1456,3 +1457,35 @@ __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_big(SampleAr
     engine<D, SCHEME, STATS>(a, W, src, C);
     flush_counters<STATS>(a, C);
 }
+
+// batched calls (girg_edges_batch): blockIdx.y is the graph; its arguments are copied into shared
+// memory once per block, and the engine is the single-graph engine
+template <int D, int SCHEME, bool STATS>
+__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_sample_b(const SampleArgs* __restrict__ args)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ SampleArgs sa;
+    if (threadIdx.x == 0) sa = args[blockIdx.y];
+    __syncthreads();
+    WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
+    Counters C = {};
+    TileSource<D, SCHEME, STATS> src;
+    engine<D, SCHEME, STATS>(sa, W, src, C);
+    flush_counters<STATS>(sa, C);
+}
+
+template <int D, int SCHEME, bool STATS>
+__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_big_b(const SampleArgs* __restrict__ args)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ SampleArgs sa;
+    if (threadIdx.x == 0) sa = args[blockIdx.y];
+    __syncthreads();
+    WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
+    Counters C = {};
+    ItemSource<D, SCHEME, STATS> src;
+    src.nit = (*sa.err & ERR_ITEMS) ? 0u : min(*sa.nitems, sa.items_cap);
+    engine<D, SCHEME, STATS>(sa, W, src, C);
+    flush_counters<STATS>(sa, C);
+}
+

@@ -54,7 +54,7 @@ def main():
     rows.append({"mode": "sequential girg_edges", "B": args.B, "ms": best, "m_total": m,
                  "edges_per_s": m / (best * 1e-3), "graphs_per_s": args.B / (best * 1e-3)})
     print(json.dumps(rows[-1]), flush=True)
-    for ns in (1, 2, 4, 8, 16, 32):
+    for ns in (0, -8):  # 0: the fused batch (one launch per kernel for all graphs); -8: per-graph pipelines
         def bat():
             return sum(e.shape[0] for e in girg.edges_batch(ws, xs, c.T, kap, seeds, caps=caps, nstreams=ns))
 
@@ -62,7 +62,8 @@ def main():
         best = min(timed(bat)[1] for _ in range(args.reps))
         mb = bat()
         assert mb == m, (mb, m)
-        rows.append({"mode": "girg_edges_batch", "nstreams": ns, "B": args.B, "ms": best, "m_total": mb,
+        rows.append({"mode": "girg_edges_batch " + ("fused" if ns >= 0 else f"per-graph pipelines x{-ns}"),
+                     "nstreams": ns, "B": args.B, "ms": best, "m_total": mb,
                      "edges_per_s": mb / (best * 1e-3), "graphs_per_s": args.B / (best * 1e-3)})
         print(json.dumps(rows[-1]), flush=True)
     if args.out:
