@@ -1411,8 +1411,23 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         pra = nra;
         ppbar = npbar;
         if (nk >= 0) {
+#if defined(GIRG_EXP_NOLOAD2) || defined(GIRG_EXP_NOLOAD1)
+#ifdef GIRG_EXP_NOLOAD1
+            if (nk == 0) {  // timing experiment only: type-I candidates without their record loads
+#else
+            if (nk > 0) {  // timing experiment only: type-II landings without their record loads
+#endif
+#pragma unroll
+                for (int k = 0; k < D; ++k) { xu[k] = 0.25 + 1e-3 * (npa & 255); xv[k] = 0.75 - 1e-3 * (npb & 255); }
+                wu = 1.5; wv = 1.5;
+            } else {
+                load_rec<D>(a, npa, xu, wu);
+                load_rec<D>(a, npb, xv, wv);
+            }
+#else
             load_rec<D>(a, npa, xu, wu);
             load_rec<D>(a, npb, xv, wv);
+#endif
             if (nk == 0) {  // type-I: the ids key the pair's uniform (R17)
                 ua = __ldg(&a.sid[npa]);
                 ub = __ldg(&a.sid[npb]);
