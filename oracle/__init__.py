@@ -46,6 +46,13 @@ class Stats(C.Structure):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}
 
 
+class HrgStats(C.Structure):
+    _fields_ = [(name, C.c_uint64) for name in ("super_edges", "nt", "violations")]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
 class Levels(C.Structure):
     _fields_ = [
         ("L", C.c_int), ("e_min", C.c_int), ("Lmax", C.c_int), ("maxCL", C.c_int),
@@ -99,6 +106,19 @@ def lib():
         L.or_index.argtypes = [dp, dp, u64, i32, d, u32p, u64p, u32p, u64p, u64]; L.or_index.restype = i32
         L.or_count_pairs.argtypes = [i32, i32, u64p, u64p, u64p, u64p]; L.or_count_pairs.restype = i32
         L.or_set_tie_hook.argtypes = [i32, d]
+        L.or_hrg_R.argtypes = [u64, d]; L.or_hrg_R.restype = d
+        L.or_hrg_points.argtypes = [u64, d, d, u64, dp, dp]; L.or_hrg_points.restype = i32
+        L.or_hrg_cosh_dist.argtypes = [d, d, d, d]; L.or_hrg_cosh_dist.restype = d
+        L.or_hrg_prob.argtypes = [d, d, d]; L.or_hrg_prob.restype = d
+        L.or_hrg_dom_weight.argtypes = [d, d]; L.or_hrg_dom_weight.restype = d
+        L.or_hrg_dom_s.argtypes = [d]; L.or_hrg_dom_s.restype = d
+        L.or_hrg_dom_weights.argtypes = [dp, u64, d, dp]; L.or_hrg_dom_weights.restype = i32
+        L.or_hrg_edges.argtypes = [dp, dp, dp, u64, d, d, u64, u32p, u64, C.POINTER(C.c_uint64), C.POINTER(HrgStats)]
+        L.or_hrg_edges.restype = i32
+        L.or_hrg_bruteforce_t0.argtypes = [dp, dp, u64, d, u32p, u64, C.POINTER(C.c_uint64)]
+        L.or_hrg_bruteforce_t0.restype = i32
+        L.or_hrg_expected_edges.argtypes = [dp, dp, u64, d, d]; L.or_hrg_expected_edges.restype = d
+        L.or_hrg_max_ratio.argtypes = [dp, dp, dp, u64, d, d]; L.or_hrg_max_ratio.restype = d
     return _lib
 
 
@@ -347,3 +367,94 @@ def count_pairs(d, depth):
     if rc:
         raise OracleError(rc)
     return [a.astype(np.int64) for a in arrs]
+
+
+# ------------------------------------------------------------------ hyperbolic random graphs --
+def hrg_R(n, C_):
+    return lib().or_hrg_R(n, float(C_))
+
+
+def hrg_points(n, alpha, C_, seed):
+    """HRG radii r[n] and torus positions x[n] = theta / (2 pi)."""
+    r = np.empty(n, dtype=np.float64)
+    x = np.empty(n, dtype=np.float64)
+    rc = lib().or_hrg_points(n, float(alpha), float(C_), C.c_uint64(seed), _dp(r), _dp(x))
+    if rc:
+        raise OracleError(rc)
+    return r, x
+
+
+def hrg_cosh_dist(ru, rv, xu, xv):
+    return lib().or_hrg_cosh_dist(ru, rv, xu, xv)
+
+
+def hrg_prob(cosh_d, R, T):
+    return lib().or_hrg_prob(cosh_d, R, T)
+
+
+def hrg_dom_weight(r, R):
+    return lib().or_hrg_dom_weight(r, R)
+
+
+def hrg_dom_s(R):
+    return lib().or_hrg_dom_s(R)
+
+
+def hrg_dom_weights(r, C_):
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    w = np.empty_like(r)
+    rc = lib().or_hrg_dom_weights(_dp(r), r.size, float(C_), _dp(w))
+    if rc:
+        raise OracleError(rc)
+    return w
+
+
+def hrg_edges(r, x, w, C_, T, seed, cap=None, with_stats=False):
+    """HRG edges through the dominating GIRG and exact thinning (R25)."""
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    n = r.size
+    cap = cap or max(1024, 16 * n)
+    while True:
+        out = np.empty((cap, 2), dtype=np.uint32)
+        m = C.c_uint64(0)
+        st = HrgStats()
+        rc = lib().or_hrg_edges(_dp(r), _dp(x), _dp(w), n, float(C_), float(T), C.c_uint64(seed), _u32p(out), cap,
+                                C.byref(m), C.byref(st))
+        if rc == ECAPACITY:
+            cap = int(m.value) + 1
+            continue
+        if rc:
+            raise OracleError(rc)
+        e = out[: m.value]
+        return (e, st.as_dict()) if with_stats else e
+
+
+def hrg_bruteforce_t0(r, x, C_):
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    cap = max(1024, 16 * r.size)
+    while True:
+        out = np.empty((cap, 2), dtype=np.uint32)
+        m = C.c_uint64(0)
+        rc = lib().or_hrg_bruteforce_t0(_dp(r), _dp(x), r.size, float(C_), _u32p(out), cap, C.byref(m))
+        if rc == ECAPACITY:
+            cap = int(m.value) + 1
+            continue
+        if rc:
+            raise OracleError(rc)
+        return out[: m.value]
+
+
+def hrg_expected_edges(r, x, C_, T):
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    return lib().or_hrg_expected_edges(_dp(r), _dp(x), r.size, float(C_), float(T))
+
+
+def hrg_max_ratio(r, x, w, C_, T):
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    return lib().or_hrg_max_ratio(_dp(r), _dp(x), _dp(w), r.size, float(C_), float(T))

@@ -269,7 +269,14 @@ int or_delta_max(uint32_t A, uint32_t B, int d, int level)
  * the bucket bounds; R6: max{l in [0, Lmax] : 2^(-d l) >= qbar_ij}, qbar_ij = (wbar_i wbar_j) s.
  * I(i): deepest CL(i,.) over nonempty partners.  R7: Lmax = min(Ln+1, floor(32/d))
  * with Ln the smallest L such that 2^(dL) >= n. */
+static int or_levels_s(const double *w, uint64_t n, int d, double kappa, double s_override, or_levels_t *lv);
 int or_levels(const double *w, uint64_t n, int d, double kappa, or_levels_t *lv)
+{
+    return or_levels_s(w, n, d, kappa, 0.0, lv);
+}
+
+/* s_override > 0 replaces s = kappa/W (the HRG's dominating GIRG fixes s itself, R25) */
+static int or_levels_s(const double *w, uint64_t n, int d, double kappa, double s_override, or_levels_t *lv)
 {
     memset(lv, 0, sizeof(*lv));
     int emin = INT_MAX, emax = INT_MIN;
@@ -285,7 +292,7 @@ int or_levels(const double *w, uint64_t n, int d, double kappa, or_levels_t *lv)
     lv->L = emax - emin + 1;
     for (uint64_t v = 0; v < n; v++) lv->cnt[ilogb(w[v]) - emin]++;
     lv->W = or_exact_sum(w, n);
-    lv->s = kappa / lv->W;
+    lv->s = s_override > 0.0 ? s_override : kappa / lv->W;
     int Ln = 0;
     while (ldexp(1.0, d * Ln) < (double)n) Ln++;
     lv->Lmax = Ln + 1 < 32 / d ? Ln + 1 : 32 / d;
@@ -778,10 +785,23 @@ static uint64_t now_ns(void)
     return (uint64_t)ts.tv_sec * 1000000000ull + (uint64_t)ts.tv_nsec;
 }
 
+static int or_run_s(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
+                    double s_override, uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi,
+                    uint32_t nranks, uint32_t rank, int scheme, uint32_t *edges, uint64_t cap,
+                    uint64_t *m_out, or_stats_t *st, uint32_t *cover, or_index_out *ix);
 static int or_run(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
                   uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi, uint32_t nranks,
                   uint32_t rank, int scheme, uint32_t *edges, uint64_t cap, uint64_t *m_out,
                   or_stats_t *st, uint32_t *cover, or_index_out *ix)
+{
+    return or_run_s(w, x, n, d, T, kappa, 0.0, seed, shard_level, blk_lo, blk_hi, nranks, rank, scheme,
+                    edges, cap, m_out, st, cover, ix);
+}
+
+static int or_run_s(const double *w, const double *x, uint64_t n, int d, double T, double kappa,
+                    double s_override, uint64_t seed, int shard_level, uint64_t blk_lo, uint64_t blk_hi,
+                    uint32_t nranks, uint32_t rank, int scheme, uint32_t *edges, uint64_t cap,
+                    uint64_t *m_out, or_stats_t *st, uint32_t *cover, or_index_out *ix)
 {
     or_stats_t dummy;
     if (!st) st = &dummy;
@@ -799,7 +819,7 @@ static int or_run(const double *w, const double *x, uint64_t n, int d, double T,
     uint64_t t0 = now_ns();
     or_ctx *c = (or_ctx *)calloc(1, sizeof(or_ctx));
     if (!c) return OR_ENOMEM;
-    int rc = or_levels(w, n, d, kappa, &c->lv);
+    int rc = or_levels_s(w, n, d, kappa, s_override, &c->lv);
     if (rc) { free(c); return rc; }
     c->w = w; c->x = x; c->n = n; c->d = d; c->T = T; c->seed = seed;
     c->invT = T > 0.0 ? 1.0 / T : 0.0;
@@ -994,6 +1014,174 @@ int or_count_pairs(int d, int depth, uint64_t *nb, uint64_t *ds, uint64_t *ds2, 
     for (int l = 0; l <= depth; l++) nb[l] = ds[l] = ds2[l] = ds3[l] = 0;
     count_rec(d, depth, 0, 0u, 0u, nb, ds, ds2, ds3);
     return OR_OK;
+}
+
+/* ===================================================================================== */
+/* Hyperbolic random graphs (Sec. 3.2) on the GIRG machinery (Sec. 3.3           */
+/* P:341-351), R25: the HRG is sampled as an exactly thinned DOMINATING GIRG.     */
+/* ===================================================================================== */
+/* R = 2 log(n) + C */
+double or_hrg_R(uint64_t n, double C) { return 2.0 * log((double)n) + C; }
+
+/* theta_v uniform in [0, 2 pi), r_v with density alpha sinh(alpha r)/(cosh(alpha R)-1)
+ * on [0, R).  Inverse transform of F(r) = (cosh(alpha r) - 1)/(cosh(alpha R) - 1):
+ * r = acosh(1 + U (cosh(alpha R) - 1)) / alpha.  Philox counter (v, 0, 0, 7): U = (o0, o1); the
+ * angle is stored as the torus position x_v = theta_v / (2 pi) = (o2, o3). */
+int or_hrg_points(uint64_t n, double alpha, double C, uint64_t seed, double *r, double *x)
+{
+    if (n < 2 || n >= (1ull << 32) || !(alpha > 0.5) || !isfinite(alpha) || !isfinite(C) || !r || !x)
+        return OR_EINVAL;
+    double R = or_hrg_R(n, C);
+    if (!(R > 0.0)) return OR_EINVAL;
+    double K = cosh(alpha * R) - 1.0;
+    for (uint64_t v = 0; v < n; v++) {
+        uint32_t ctr[4] = {(uint32_t)v, 0u, 0u, 7u}, o[4];
+        or_philox4x32_10(ctr, seed, o);
+        double U = or_u53(o[0], o[1]);
+        r[v] = acosh(1.0 + U * K) / alpha;
+        x[v] = or_u53(o[2], o[3]);
+    }
+    return OR_OK;
+}
+
+/* cosh d(p_u, p_v) = cosh r_u cosh r_v - sinh r_u sinh r_v cos(dtheta), dtheta the
+ * angular distance in [0, pi] = 2 pi * (torus distance of x_u, x_v) */
+double or_hrg_cosh_dist(double ru, double rv, double xu, double xv)
+{
+    double a = fabs(xu - xv);
+    double t = a < 1.0 - a ? a : 1.0 - a;
+    return cosh(ru) * cosh(rv) - sinh(ru) * sinh(rv) * cos(6.283185307179586 * t);
+}
+
+/* T = 0: edge iff d < R, i.e. cosh d < cosh R; T > 0: p_T(d) = 1/(exp((d-R)/(2T)) + 1) */
+double or_hrg_prob(double cosh_d, double R, double T)
+{
+    if (T == 0.0) return cosh_d < cosh(R) ? 1.0 : 0.0;
+    double d = acosh(cosh_d < 1.0 ? 1.0 : cosh_d);
+    return 1.0 / (exp((d - R) / (2.0 * T)) + 1.0);
+}
+
+/* R25 dominating weight: w'_v = e^((R - r_v)/2) / sqrt(1 - e^(-2 r_v)) (the GIRG weight of P:345
+ * divided by sqrt(2 sinh(r_v) e^(-r_v))), and e^(R/2) at r_v = 0 (then every GIRG' pair of v
+ * saturates).  With s' = e^(-R/2)/sqrt(2) every HRG probability is at most the GIRG one:
+ * cosh d >= 2 sinh r_u sinh r_v sin^2(pi dx) >= 2 e^(2R) dx^2 / (w'_u w'_v)^2, so e^(-d) <=
+ * 1/cosh d gives p_T(d) <= e^((R-d)/(2T)) <= (w'_u w'_v s' / dx)^(1/T), and d < R gives
+ * dx < w'_u w'_v s'. */
+double or_hrg_dom_weight(double r, double R)
+{
+    if (r <= 0.0) return exp(0.5 * R);
+    return exp(0.5 * (R - r)) / sqrt(-expm1(-2.0 * r));
+}
+
+double or_hrg_dom_s(double R) { return exp(-0.5 * R) / sqrt(2.0) * (1.0 + 0x1p-30); }
+
+int or_hrg_dom_weights(const double *r, uint64_t n, double C, double *w)
+{
+    if (!r || !w || n < 2) return OR_EINVAL;
+    double R = or_hrg_R(n, C);
+    for (uint64_t v = 0; v < n; v++) w[v] = or_hrg_dom_weight(r[v], R);
+    return OR_OK;
+}
+
+/* The HRG edge set: the dominating GIRG (w', x, d = 1, T, s') sampled by the GIRG sampler (merged
+ * scheme, the same keyed randomness), then every GIRG edge kept with probability p_HRG / p_GIRG
+ * (T > 0: uniform from Philox counter (u, v, 0, 6), u < v, words (o0, o1), kept iff r < ratio;
+ * T = 0: kept iff cosh d < cosh R).  Each pair is an edge with probability
+ * p_GIRG * p_HRG / p_GIRG = p_HRG, independently: the HRG distribution exactly.
+ * Near-ties (north-star rule) of the thinning decision: |r - ratio| < 1e-12 (T > 0),
+ * |cosh d - cosh R| < 1e-12 cosh R (T = 0); dominance violations (ratio > 1) counted. */
+int or_hrg_edges(const double *r, const double *x, const double *w, uint64_t n, double C, double T,
+                 uint64_t seed, uint32_t *edges, uint64_t cap, uint64_t *m_out, or_hrg_stats_t *hst)
+{
+    or_hrg_stats_t dummy;
+    if (!hst) hst = &dummy;
+    memset(hst, 0, sizeof(*hst));
+    if (!r || !x || !w || !m_out || (cap && !edges) || n < 2) return OR_EINVAL;
+    if (!(T >= 0.0 && T < 1.0)) return OR_EINVAL;
+    double R = or_hrg_R(n, C), sd = or_hrg_dom_s(R), coshR = cosh(R);
+    uint64_t scap = 16 * n + 1024, sm = 0;
+    uint32_t *sup = NULL;
+    int rc;
+    for (;;) {
+        sup = (uint32_t *)malloc(sizeof(uint32_t) * 2 * scap);
+        if (!sup) return OR_ENOMEM;
+        rc = or_run_s(w, x, n, 1, T, 1.0, sd, seed, 0, 0, 1, 0, 0, OR_SCHEME_MERGED, sup, scap, &sm, NULL,
+                      NULL, NULL);
+        if (rc != OR_ECAPACITY) break;
+        free(sup);
+        scap = sm + 1;
+    }
+    if (rc) { free(sup); return rc; }
+    hst->super_edges = sm;
+    uint64_t m = 0;
+    for (uint64_t k = 0; k < sm; k++) {
+        uint32_t u = sup[2 * k], v = sup[2 * k + 1];
+        double cd = or_hrg_cosh_dist(r[u], r[v], x[u], x[v]);
+        int keep;
+        if (T == 0.0) {
+            if (fabs(cd - coshR) < 1e-12 * coshR) hst->nt++;
+            keep = cd < coshR;
+        } else {
+            double ph = or_hrg_prob(cd, R, T);
+            double a = fabs(x[u] - x[v]);
+            double D = a < 1.0 - a ? a : 1.0 - a; /* d = 1: D = dist */
+            double pg = or_prob(w[u], w[v], sd, D, T);
+            double ratio = ph / pg;
+            if (ratio > 1.0) hst->violations++;
+            uint32_t ctr[4] = {u < v ? u : v, u < v ? v : u, 0u, 6u}, o[4];
+            or_philox4x32_10(ctr, seed, o);
+            double rr = or_u53(o[0], o[1]);
+            if (fabs(rr - ratio) < 1e-12) hst->nt++;
+            keep = rr < ratio;
+        }
+        if (keep) {
+            if (m < cap) { edges[2 * m] = u; edges[2 * m + 1] = v; }
+            m++;
+        }
+    }
+    free(sup);
+    *m_out = m;
+    return m > cap ? OR_ECAPACITY : OR_OK;
+}
+
+/* O(n^2) definitions: threshold HRG edge set (d < R), the expected edge count sum p_T(d), and
+ * the largest p_HRG / p_GIRG' over all pairs (dominance, must be <= 1) */
+int or_hrg_bruteforce_t0(const double *r, const double *x, uint64_t n, double C, uint32_t *edges, uint64_t cap,
+                         uint64_t *m_out)
+{
+    double coshR = cosh(or_hrg_R(n, C));
+    uint64_t m = 0;
+    for (uint64_t u = 0; u < n; u++)
+        for (uint64_t v = u + 1; v < n; v++)
+            if (or_hrg_cosh_dist(r[u], r[v], x[u], x[v]) < coshR) {
+                if (m < cap) { edges[2 * m] = (uint32_t)u; edges[2 * m + 1] = (uint32_t)v; }
+                m++;
+            }
+    *m_out = m;
+    return m > cap ? OR_ECAPACITY : OR_OK;
+}
+
+double or_hrg_expected_edges(const double *r, const double *x, uint64_t n, double C, double T)
+{
+    double R = or_hrg_R(n, C), acc = 0.0;
+    for (uint64_t u = 0; u < n; u++)
+        for (uint64_t v = u + 1; v < n; v++) acc += or_hrg_prob(or_hrg_cosh_dist(r[u], r[v], x[u], x[v]), R, T);
+    return acc;
+}
+
+double or_hrg_max_ratio(const double *r, const double *x, const double *w, uint64_t n, double C, double T)
+{
+    double R = or_hrg_R(n, C), sd = or_hrg_dom_s(R), best = 0.0;
+    for (uint64_t u = 0; u < n; u++)
+        for (uint64_t v = u + 1; v < n; v++) {
+            double a = fabs(x[u] - x[v]);
+            double D = a < 1.0 - a ? a : 1.0 - a;
+            double ph = or_hrg_prob(or_hrg_cosh_dist(r[u], r[v], x[u], x[v]), R, T);
+            double pg = T == 0.0 ? (double)or_thresh_edge(w[u], w[v], sd, D) : or_prob(w[u], w[v], sd, D, T);
+            double ratio = ph == 0.0 ? 0.0 : (pg == 0.0 ? INFINITY : ph / pg);
+            if (ratio > best) best = ratio;
+        }
+    return best;
 }
 
 /* ===================================================================================== */

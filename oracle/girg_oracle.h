@@ -109,6 +109,27 @@ int or_index(const double *w, const double *x, uint64_t n, int d, double kappa, 
              uint64_t *lstart, uint32_t *P, uint64_t *poff, uint64_t pcap);
 int or_count_pairs(int d, int depth, uint64_t *nb, uint64_t *ds, uint64_t *ds2, uint64_t *ds3);
 
+/* ---- hyperbolic random graphs, Sec. 3.2, through the dominating GIRG of Sec. 3.3
+ * P:341-351 and exact thinning (R25) ---- */
+typedef struct {
+    uint64_t super_edges; /* edges of the dominating GIRG */
+    uint64_t nt;          /* thinning near-ties (must be 0) */
+    uint64_t violations;  /* pairs with p_HRG > p_GIRG' (must be 0) */
+} or_hrg_stats_t;
+double or_hrg_R(uint64_t n, double C);
+int or_hrg_points(uint64_t n, double alpha, double C, uint64_t seed, double *r, double *x);
+double or_hrg_cosh_dist(double ru, double rv, double xu, double xv);
+double or_hrg_prob(double cosh_d, double R, double T);
+double or_hrg_dom_weight(double r, double R);
+double or_hrg_dom_s(double R);
+int or_hrg_dom_weights(const double *r, uint64_t n, double C, double *w);
+int or_hrg_edges(const double *r, const double *x, const double *w, uint64_t n, double C, double T,
+                 uint64_t seed, uint32_t *edges, uint64_t cap, uint64_t *m_out, or_hrg_stats_t *hst);
+int or_hrg_bruteforce_t0(const double *r, const double *x, uint64_t n, double C, uint32_t *edges,
+                         uint64_t cap, uint64_t *m_out);
+double or_hrg_expected_edges(const double *r, const double *x, uint64_t n, double C, double T);
+double or_hrg_max_ratio(const double *r, const double *x, const double *w, uint64_t n, double C, double T);
+
 /* O(n^2) brute force, threshold model (T=0), canonical arithmetic */
 int or_bruteforce_t0(const double *w, const double *x, uint64_t n, int d, double kappa,
                      uint32_t *edges, uint64_t cap, uint64_t *m_out);
