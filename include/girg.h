@@ -194,6 +194,45 @@ int girg_edges_batch(int B, const double *const *w_dev, const double *const *x_d
                      uint32_t *const *edges_dev, const uint64_t *cap, uint64_t *m_out,
                      int *status_out, int nstreams, void *stream);
 
+/*
+ * Hyperbolic random graphs (Sec. 3.2) on the GIRG machinery (Sec. 3.3
+ * P:341-351; R25).
+ *
+ * girg_hrg_points -- n HRG points: radius r_v with density alpha sinh(alpha r)/(cosh(alpha R)-1)
+ * on [0, R), R = 2 ln(n) + C, by inverse transform of the 53-bit uniform U of Philox
+ * counter (v, 0, 0, 7) words (o0, o1): r = acosh(1 + U (cosh(alpha R) - 1)) / alpha; the angle as
+ * the torus position x_v = theta_v / (2 pi) = words (o2, o3); and the dominating GIRG
+ * weight w'_v = e^((R - r_v)/2) / sqrt(1 - e^(-2 r_v)) (e^(R/2) at r_v = 0).  Outputs r_dev[n],
+ * x_dev[n], w_dev[n] (float64, caller-owned device buffers).  Asynchronous.
+ * Errors: EINVAL if n < 2, n >= 2^32, alpha <= 1/2 or not finite, C not finite, R <= 0, a NULL
+ * pointer; ERANGE if cosh(alpha R) overflows.
+ */
+int girg_hrg_points(uint64_t n, double alpha, double C, uint64_t seed, double *r_dev, double *x_dev,
+                    double *w_dev, void *stream);
+
+typedef struct {
+    uint64_t super_edges; /* edges of the dominating GIRG                                  */
+    uint64_t neartie;     /* thinning decisions within 1e-12 of their threshold (must be 0) */
+    uint64_t violations;  /* pairs with p_HRG > p_GIRG' (must be 0)                         */
+} girg_hrg_stats;
+
+/*
+ * girg_hrg_edges -- the HRG edge set of points (r_dev, x_dev) with dominating weights w_dev
+ * (girg_hrg_points), R = 2 ln(n) + C, temperature T in [0, 1): T = 0 threshold model, edge iff
+ * the hyperbolic distance d < R; T > 0 binomial model, p_T(d) = 1/(exp((d-R)/(2T))+1)
+ * (P:316-318); cosh d = cosh r_u cosh r_v - sinh r_u sinh r_v cos(2 pi dx).
+ * Sampled exactly as girg_edges of the dominating GIRG (w', x, d = 1, T, s = e^(-R/2)/sqrt(2)
+ * (1 + 2^-30) instead of kappa/W, merged scheme, `seed`) thinned by p_HRG / p_GIRG' (uniform of
+ * Philox counter (u, v, 0, 6), u < v; T = 0: the exact test cosh d < cosh R).  Output as
+ * girg_edges: edges_dev[cap][2] uint32 (u < v), *m_out, ECAPACITY when m > cap (then re-run with
+ * cap >= m: identical set).  stats_out may be NULL.  Synchronises `stream`.
+ * Errors: EINVAL (NULL pointer, n < 2, T not in [0,1), C not finite, R <= 0), ECAPACITY, ENOMEM,
+ * ECUDA, and the errors of girg_edges for the dominating GIRG (e.g. ERANGE for > 64 layers).
+ */
+int girg_hrg_edges(const double *r_dev, const double *x_dev, const double *w_dev, uint64_t n,
+                   double C, double T, uint64_t seed, uint32_t *edges_dev, uint64_t cap,
+                   uint64_t *m_out, girg_hrg_stats *stats_out, void *stream);
+
 /* Phase timings of the last successful girg_edges / girg_edges_shard / girg_edges_host call on
  * the calling host thread, measured with CUDA events recorded on the call's stream around each
  * phase (the events cost ~1 us; they are always recorded). */

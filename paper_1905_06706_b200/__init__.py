@@ -67,15 +67,19 @@ _lib.girg_edges_ex.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, C.POINTER(Optio
 _lib.girg_edges_host.argtypes = [_vp, _vp, _u64, _i, _d, _d, _u64, _vp, _u64, C.POINTER(_u64), _vp]
 _lib.girg_edges_batch.argtypes = [_i, _vp, _vp, _u64, _i, _d, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp]
 _lib.girg_last_timings.argtypes = [C.POINTER(Timings)]
+_lib.girg_hrg_points.argtypes = [_u64, _d, _d, _u64, _vp, _vp, _vp, _vp]
+_lib.girg_hrg_edges.argtypes = [_vp, _vp, _vp, _u64, _d, _d, _u64, _vp, _u64, C.POINTER(_u64), C.c_void_p, _vp]
 _lib.girg_strerror.argtypes = [_i]
 _lib.girg_strerror.restype = C.c_char_p
 _lib.girg_last_cuda_error.restype = C.c_char_p
 for _f in ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
-           "girg_edges_ex", "girg_edges_host", "girg_edges_batch", "girg_version", "girg_last_timings"):
+           "girg_edges_ex", "girg_edges_host", "girg_edges_batch", "girg_version", "girg_last_timings",
+           "girg_hrg_points", "girg_hrg_edges"):
     getattr(_lib, _f).restype = C.c_int
 
 EXPORTS = ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
-           "girg_edges_ex", "girg_edges_host", "girg_edges_batch", "girg_strerror", "girg_last_cuda_error", "girg_version", "girg_last_timings")
+           "girg_edges_ex", "girg_edges_host", "girg_edges_batch", "girg_strerror", "girg_last_cuda_error", "girg_version",
+           "girg_last_timings", "girg_hrg_points", "girg_hrg_edges")
 
 
 class GirgError(RuntimeError):
@@ -240,6 +244,48 @@ def edges_batch(ws, xs, T: float, kappas, seeds, caps=None, nstreams: int = 8, s
     if rc not in (0, ECAPACITY):
         _check(rc)
     return out
+
+
+class HrgStats(C.Structure):
+    _fields_ = [("super_edges", C.c_uint64), ("neartie", C.c_uint64), ("violations", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
+def hrg_points(n: int, alpha: float, C_: float, seed: int, stream=None):
+    """HRG points (include/girg.h girg_hrg_points): radii r, torus positions x = theta/(2 pi) and
+    the dominating GIRG weights w' (float64 CUDA tensors [n])."""
+    r = torch.empty(n, dtype=torch.float64, device="cuda")
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    w = torch.empty(n, dtype=torch.float64, device="cuda")
+    _check(_lib.girg_hrg_points(n, alpha, C_, seed, r.data_ptr(), x.data_ptr(), w.data_ptr(), _stream(stream)))
+    return r, x, w
+
+
+def hrg_edges(r: torch.Tensor, x: torch.Tensor, w: torch.Tensor, C_: float, T: float, seed: int,
+              cap: int | None = None, stats: bool = False, stream=None):
+    """HRG edge list (include/girg.h girg_hrg_edges): int32 CUDA tensor [m, 2] of uint32 pairs u < v."""
+    for t, nm in ((r, "r"), (x, "x"), (w, "w")):
+        _dev_f64(t, nm)
+    n = r.numel()
+    if x.numel() != n or w.numel() != n:
+        raise ValueError("r, x, w must have n elements each")
+    cap = cap if cap is not None else 16 * n + 1024
+    with torch.cuda.device(r.device):
+        for _ in range(2):
+            buf = torch.empty((cap, 2), dtype=torch.int32, device=r.device)
+            m = C.c_uint64(0)
+            st = HrgStats()
+            rc = _lib.girg_hrg_edges(r.data_ptr(), x.data_ptr(), w.data_ptr(), n, C_, T, seed, buf.data_ptr(), cap,
+                                     C.byref(m), C.cast(C.pointer(st), C.c_void_p), _stream(stream))
+            if rc == ECAPACITY:
+                cap = int(m.value)
+                continue
+            _check(rc)
+            e = buf[: m.value]
+            return (e, st.as_dict()) if stats else e
+    raise GirgError(ECAPACITY)
 
 
 def last_timings() -> dict:

@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = [os.path.join(HERE, "csrc", "girg.cu")]
-DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("girg_device.cuh", "sample.cuh")] + [
+DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("girg_device.cuh", "sample.cuh", "hrg.cuh")] + [
     os.path.join(ROOT, "include", "girg.h")]
 LIB = os.path.join(HERE, "libgirg.so")
 DEBUG_LIB = os.path.join(HERE, "libgirg_debug.so")  # bounds-checked build (-DGIRG_DEBUG)

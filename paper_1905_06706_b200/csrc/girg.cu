@@ -702,7 +702,7 @@ struct HostPlan {
 
 // H6: layers, levels and bound tables; R5-R7, R9, R10.
 static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WPartial>& parts, uint64_t n, int d,
-                     double T, double kappa, HostPlan& hp)
+                     double T, double kappa, HostPlan& hp, double s_override = 0.0)
 {
     Plan& p = hp.p;
     std::memset(&p, 0, sizeof(p));
@@ -720,7 +720,7 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
     p.e_min = emin;
     p.T = T;
     p.invT = T > 0.0 ? 1.0 / T : 0.0;
-    p.s = kappa / hp.W;
+    p.s = s_override > 0.0 ? s_override : kappa / hp.W;  // s_override: the HRG's dominating GIRG (R25)
     for (int i = 0; i < p.L; ++i) p.cnt[i] = hist[emin + i + EXP_BIAS];
     int Ln = 0;
     while (std::ldexp(1.0, d * Ln) < (double)n) ++Ln;
@@ -984,6 +984,7 @@ struct EdgeCall {
     int sl;
     uint64_t blo, bhi;
     uint32_t nranks = 0, rank = 0;  // interleaved ownership (nranks > 0) instead of a block range
+    double s_override = 0.0;        // > 0: s fixed instead of kappa / W (HRG's dominating GIRG, R25)
     int scheme;
     uint32_t* edges;
     uint64_t cap;
@@ -1052,7 +1053,7 @@ struct EdgeCall {
         std::memcpy(parts.data(), wst_host + HIST_BINS * sizeof(uint32_t) + 16, nb * sizeof(WPartial));
         if (herr & ERR_WEIGHT) { rc = GIRG_EINVAL; return; }
         if (herr & ERR_WRANGE) { rc = GIRG_ERANGE; return; }
-        rc = make_plan(hist, parts, n, d, T, kappa, hp);
+        rc = make_plan(hist, parts, n, d, T, kappa, hp, s_override);
         if (rc) return;
         hp.p.sl = sl;
         hp.p.blo = blo;
@@ -1227,7 +1228,7 @@ struct EdgeCall {
 static int edges_impl(const double* w, const double* x, uint64_t n, int d, double T, double kappa,
                       uint64_t seed, int sl, uint64_t blo, uint64_t bhi, int scheme, uint32_t* edges, uint64_t cap,
                       uint64_t* m_out, girg_stats* stats_out, cudaStream_t st, uint32_t nranks = 0,
-                      uint32_t rank = 0)
+                      uint32_t rank = 0, double s_override = 0.0)
 {
     if (nranks > 0) {  // interleaved ownership: the block range is unused
         if (rank >= nranks) return GIRG_EINVAL;
@@ -1240,6 +1241,7 @@ static int edges_impl(const double* w, const double* x, uint64_t n, int d, doubl
         EdgeCall E(w, x, n, d, T, kappa, seed, sl, blo, bhi, scheme, edges, cap, m_out, stats_out, st);
         E.nranks = nranks;
         E.rank = rank;
+        E.s_override = s_override;
         E.stage_a();
         GCHECK(cudaStreamSynchronize(st));
         E.stage_b();
@@ -1680,6 +1682,8 @@ static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double
         return GIRG_ECUDA;
     }
 }
+
+#include "hrg.cuh"
 
 }  // namespace girg
 
@@ -2135,6 +2139,20 @@ extern "C" int girg_edges_batch(int B, const double* const* w_dev, const double*
         if (rc == GIRG_OK && status[g] != GIRG_OK) rc = status[g];
     }
     return rc;
+}
+
+extern "C" int girg_hrg_points(uint64_t n, double alpha, double C, uint64_t seed, double* r_dev, double* x_dev,
+                               double* w_dev, void* stream)
+{
+    return girg::hrg_points_impl(n, alpha, C, seed, r_dev, x_dev, w_dev, (cudaStream_t)stream);
+}
+
+extern "C" int girg_hrg_edges(const double* r_dev, const double* x_dev, const double* w_dev, uint64_t n, double C,
+                              double T, uint64_t seed, uint32_t* edges_dev, uint64_t cap, uint64_t* m_out,
+                              girg_hrg_stats* stats_out, void* stream)
+{
+    return girg::hrg_edges_impl(r_dev, x_dev, w_dev, n, C, T, seed, edges_dev, cap, m_out, stats_out,
+                                (cudaStream_t)stream);
 }
 
 extern "C" const char* girg_strerror(int status)
