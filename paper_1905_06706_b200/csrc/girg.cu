@@ -891,23 +891,39 @@ static void smem_optin(K kern, size_t bytes)
     done.emplace_back(dev, f);
 }
 
-template <int D, int SCHEME, bool STATS>
+// the sampling kernel pair of an instantiation: the engine (T > 0) or the flat T = 0 loop
+template <int D, int SCHEME, bool STATS, bool T0>
+struct SampleKernels {
+    static constexpr auto sample()
+    {
+        if constexpr (T0) return k_sample_t0<D, STATS>;
+        else return k_sample<D, SCHEME, STATS>;
+    }
+    static constexpr auto big()
+    {
+        if constexpr (T0) return k_big_t0<D, STATS>;
+        else return k_big<D, SCHEME, STATS>;
+    }
+};
+
+template <int D, int SCHEME, bool STATS, bool T0 = false>
 static void launch_sample_t(const SampleArgs& a, cudaStream_t st)
 {
+    using SK = SampleKernels<D, SCHEME, STATS, T0>;
     constexpr int WPB = Geo<D>::WPB, TPB = 32 * WPB;
     const size_t smem = sizeof(WarpSmem<D>) * WPB;
-    smem_optin(k_sample<D, SCHEME, STATS>, smem);
-    smem_optin(k_big<D, SCHEME, STATS>, smem);
+    smem_optin(SK::sample(), smem);
+    smem_optin(SK::big(), smem);
     // SM count and occupancies queried once per instantiation (one GPU type per process)
     const int nsm = device_sms();
     static const int occ = [] {
         int v = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_sample<D, SCHEME, STATS>, TPB, sizeof(WarpSmem<D>) * WPB);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, SK::sample(), TPB, sizeof(WarpSmem<D>) * WPB);
         return v;
     }();
     static const int occ2 = [] {
         int v = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_big<D, SCHEME, STATS>, TPB, sizeof(WarpSmem<D>) * WPB);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, SK::big(), TPB, sizeof(WarpSmem<D>) * WPB);
         return v;
     }();
     const unsigned wtiles = (a.ntiles + WPB - 1) / WPB;
@@ -924,7 +940,7 @@ static void launch_sample_t(const SampleArgs& a, cudaStream_t st)
         GCHECK(cudaMallocAsync(&b.wprof, 2 * nwarps * 4 * sizeof(unsigned long long), st));
         GCHECK(cudaMemsetAsync(b.wprof, 0, 2 * nwarps * 4 * sizeof(unsigned long long), st));
     }
-    k_sample<D, SCHEME, STATS><<<grid, TPB, smem, st>>>(b);
+    SK::sample()<<<grid, TPB, smem, st>>>(b);
     GCHECK(cudaGetLastError());
     if (sync_debug) {
         cudaError_t e = cudaStreamSynchronize(st);
@@ -933,7 +949,7 @@ static void launch_sample_t(const SampleArgs& a, cudaStream_t st)
         GCHECK(e);
     }
     if (b.wprof) b.wprof += nwarps * 4;
-    k_big<D, SCHEME, STATS><<<gbig, TPB, smem, st>>>(b);
+    SK::big()<<<gbig, TPB, smem, st>>>(b);
     GCHECK(cudaGetLastError());
     if (wprof_path) {
         std::vector<unsigned long long> h(2 * nwarps * 4);
@@ -958,7 +974,10 @@ static void launch_sample_t(const SampleArgs& a, cudaStream_t st)
 template <int D>
 static void launch_sample(const SampleArgs& a, int scheme, cudaStream_t st)
 {
-    if (scheme == SCHEME_EVENT) {
+    if (a.T == 0.0) {  // threshold model: no type-II events in either scheme, the flat loop
+        if (a.stats) launch_sample_t<D, SCHEME_MERGED, true, true>(a, st);
+        else launch_sample_t<D, SCHEME_MERGED, false, true>(a, st);
+    } else if (scheme == SCHEME_EVENT) {
         if (a.stats) launch_sample_t<D, SCHEME_EVENT, true>(a, st);
         else launch_sample_t<D, SCHEME_EVENT, false>(a, st);
     } else {

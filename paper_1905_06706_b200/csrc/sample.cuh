@@ -1448,6 +1448,55 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
 #endif
 }
 
+// T = 0 (threshold model: every unit is a type-I candidate, no jump chains, no draws): a flat
+// candidate loop -- 32 candidates per warp step, one per lane -- in its own kernel instantiation
+// (FLAT = true), so the T > 0 engine's register allocation is untouched.  B200, sampling phase:
+// n = 2^24 d = 1 11.4 -> 10.9 ms, n = 2^22 d = 2 8.3 -> 6.2 ms, n = 2^20 d = 3 5.9 -> 5.5 ms.
+template <int D, int SCHEME, bool STATS, class Src>
+__device__ __forceinline__ void engine_cand(const SampleArgs& a, WarpSmem<D>& W, Src& src, Counters& C)
+{
+    const unsigned lane = lane_id();
+    unsigned fill = 0;
+    const double s_ = a.s;
+    for (;;) {
+        unsigned long long lo, hi;
+        if (!src.next(a, W.slot[0], lo, hi, C)) break;
+        const SlotT<D>& S = W.slot[0];
+        for (unsigned long long b = lo; b < hi; b += 32) {
+            const unsigned long long u = b + lane;
+            bool edge = false;
+            uint32_t ua = 0, ub = 0;
+            if (u < hi) {
+                int q = 0;
+                while (q < 3 * Geo<D>::CB - 1 && S.uoff[q + 1] <= u) ++q;
+                const int qc = q / 3;
+                const Seq& Q = S.seq[qc][0];
+                uint32_t ti;
+                const uint32_t si = divmod(u - S.uoff[q], Q.M, ti);
+                uint32_t B;
+                const uint32_t npa = Q.a0 + si;
+                const uint32_t npb = locate(S, S.job.npar, S.job.cs, qc, 0, ti, B);
+                if (!(S.job.same_layer && B == Q.A && npb <= npa)) {
+                    double xu[D], xv[D], wu, wv;
+                    load_rec<D>(a, npa, xu, wu);
+                    load_rec<D>(a, npb, xv, wv);
+                    edge = dist_pow<D>(xu, xv) <= __dmul_rn(__dmul_rn(wu, wv), s_);
+                    if (STATS) {
+                        ++C.cand1;
+                        C.edges1 += edge;
+                    }
+                    if (edge) {
+                        ua = __ldg(&a.sid[npa]);
+                        ub = __ldg(&a.sid[npb]);
+                    }
+                }
+            }
+            warp_emit<Geo<D>::EB>(a, W.ebuf, fill, edge, ua, ub);
+        }
+    }
+    warp_flush(a, W.ebuf, fill);
+}
+
 template <int D, int SCHEME, bool STATS>
 __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_sample(SampleArgs a)
 {
@@ -1456,6 +1505,30 @@ __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_sample(Sampl
     Counters C = {};
     TileSource<D, SCHEME, STATS> src;
     engine<D, SCHEME, STATS>(a, W, src, C);
+    flush_counters<STATS>(a, C);
+}
+
+// T = 0 instantiations (flat candidate loop)
+template <int D, bool STATS>
+__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_sample_t0(SampleArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
+    Counters C = {};
+    TileSource<D, SCHEME_MERGED, STATS> src;
+    engine_cand<D, SCHEME_MERGED, STATS>(a, W, src, C);
+    flush_counters<STATS>(a, C);
+}
+
+template <int D, bool STATS>
+__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_big_t0(SampleArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
+    Counters C = {};
+    ItemSource<D, SCHEME_MERGED, STATS> src;
+    src.nit = (*a.err & ERR_ITEMS) ? 0u : min(*a.nitems, a.items_cap);
+    engine_cand<D, SCHEME_MERGED, STATS>(a, W, src, C);
     flush_counters<STATS>(a, C);
 }
 
