@@ -34,6 +34,10 @@
 #include "../../include/girg.h"
 #include "girg_device.cuh"
 
+#ifndef GIRG_CHUNK_SHIFT
+#define GIRG_CHUNK_SHIFT 1  // merged chunks of 2^(SHIFT - ilogb(pbar)) candidates (R22; the oracle's value)
+#endif
+
 namespace girg {
 
 constexpr int MAXL = 64;
@@ -775,7 +779,7 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
                         int c2 = 0, c2m = 0;
                         if (e.pbar > 0.0) {
                             c2 = std::min(62, std::max(0, 1 - std::ilogb(e.pbar)));   // R10
-                            c2m = std::min(62, std::max(0, 1 - std::ilogb(e.pbar)));  // R22
+                            c2m = std::min(62, std::max(0, GIRG_CHUNK_SHIFT - std::ilogb(e.pbar)));  // R22
                         }
                         e.clog2 = c2;
                         e.clog2m = c2m;
