@@ -106,6 +106,9 @@ def lib():
         L.or_index.argtypes = [dp, dp, u64, i32, d, u32p, u64p, u32p, u64p, u64]; L.or_index.restype = i32
         L.or_count_pairs.argtypes = [i32, i32, u64p, u64p, u64p, u64p]; L.or_count_pairs.restype = i32
         L.or_set_tie_hook.argtypes = [i32, d]
+        L.or_det_log.argtypes = [d]; L.or_det_log.restype = d
+        L.or_det_exp.argtypes = [d]; L.or_det_exp.restype = d
+        L.or_det_pow.argtypes = [d, d]; L.or_det_pow.restype = d
         L.or_hrg_R.argtypes = [u64, d]; L.or_hrg_R.restype = d
         L.or_hrg_points.argtypes = [u64, d, d, u64, dp, dp]; L.or_hrg_points.restype = i32
         L.or_hrg_cosh_dist.argtypes = [d, d, d, d]; L.or_hrg_cosh_dist.restype = d
@@ -312,6 +315,18 @@ def scale_weights(w, avg_deg, d, T, beta) -> float:
 
 def geometric_skip(p, u) -> int:
     return int(lib().or_geometric_skip(p, u))
+
+
+def det_log(x):
+    return lib().or_det_log(float(x))
+
+
+def det_exp(t):
+    return lib().or_det_exp(float(t))
+
+
+def det_pow(x, y):
+    return lib().or_det_pow(float(x), float(y))
 
 
 def set_tie_hook(mode: int, delta: float = 0.0):

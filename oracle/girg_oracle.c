@@ -72,6 +72,98 @@ void or_set_tie_hook(int mode, double delta)
 /* Model, Sec. 2.1                                                           */
 /* ===================================================================================== */
 
+/* ===================================================================================== */
+/* R26: the canonical log / exp / pow of the edge decisions.  Written with + - * / and bit   */
+/* operations only (no libm), so the oracle and the CUDA library (which implements the same */
+/* formulas independently) compute identical bits: T > 0 decisions cannot differ by a libm   */
+/* ulp any more.  Accuracy (pinned against glibc by tests/test_oracle_model.py): log within */
+/* 2 ulp, exp within 2 ulp, pow within 1e-13 relative over the decisions' range.            */
+/* ===================================================================================== */
+static const double OR_LN2_HI = 0x1.62e42fee00000p-1; /* 21 trailing zero bits: k*LN2_HI exact */
+static const double OR_LN2_LO = 0x1.a39ef35793c76p-33;
+
+static double or_pow2i(int k) /* 2^k for -1022 <= k <= 1023 */
+{
+    uint64_t b = (uint64_t)(k + 1023) << 52;
+    double r;
+    memcpy(&r, &b, 8);
+    return r;
+}
+
+/* log x, x > 0 finite: x = m 2^k, m in [sqrt(1/2), sqrt(2)); s = (m-1)/(m+1);
+ * log m = 2 atanh(s) = 2 s (1 + s^2/3 + s^4/5 + ... + s^22/23) (|s| <= 0.172, the next term is
+ * below 2^-60 relative); log x = k ln2_hi + (k ln2_lo + log m) */
+double or_det_log(double x)
+{
+    if (!(x > 0.0)) return x == 0.0 ? -INFINITY : NAN;
+    if (isinf(x)) return x;
+    int k = 0;
+    uint64_t b;
+    memcpy(&b, &x, 8);
+    if (((b >> 52) & 0x7ff) == 0) { /* subnormal: scale into the normal range */
+        x = x * 0x1p54;
+        k = -54;
+        memcpy(&b, &x, 8);
+    }
+    k += (int)((b >> 52) & 0x7ff) - 1023;
+    b = (b & 0x000fffffffffffffull) | 0x3ff0000000000000ull;
+    double m;
+    memcpy(&m, &b, 8); /* m in [1, 2) */
+    if (m > 0x1.6a09e667f3bcdp+0) { /* sqrt(2) */
+        m = m * 0.5;
+        k += 1;
+    }
+    double f = m - 1.0;
+    double s = f / (m + 1.0);
+    double z = s * s;
+    double p = 0x1.642c8590b2164p-5;        /* 1/23 */
+    p = p * z + 0x1.8618618618618p-5;       /* 1/21 */
+    p = p * z + 0x1.af286bca1af28p-5;       /* 1/19 */
+    p = p * z + 0x1.e1e1e1e1e1e1ep-5;       /* 1/17 */
+    p = p * z + 0x1.1111111111111p-4;       /* 1/15 */
+    p = p * z + 0x1.3b13b13b13b14p-4;       /* 1/13 */
+    p = p * z + 0x1.745d1745d1746p-4;       /* 1/11 */
+    p = p * z + 0x1.c71c71c71c71cp-4;       /* 1/9 */
+    p = p * z + 0x1.2492492492492p-3;       /* 1/7 */
+    p = p * z + 0x1.999999999999ap-3;       /* 1/5 */
+    p = p * z + 0x1.5555555555555p-2;       /* 1/3 */
+    double logm = (2.0 * s) + (2.0 * s) * (z * p);
+    double kd = (double)k;
+    return kd * OR_LN2_HI + (kd * OR_LN2_LO + logm);
+}
+
+/* exp t: k = round-half-even(t / ln2), r = (t - k ln2_hi) - k ln2_lo (|r| <= 0.35),
+ * exp r = sum_{i <= 13} r^i / i! (Horner), times 2^k (two exact-or-IEEE-rounded multiplies) */
+double or_det_exp(double t)
+{
+    if (isnan(t)) return t;
+    if (t > 709.78) return INFINITY;
+    if (t < -745.2) return 0.0;
+    double kd = nearbyint(t * 0x1.71547652b82fep+0); /* 1/ln2 */
+    int k = (int)kd;
+    double r = (t - kd * OR_LN2_HI) - kd * OR_LN2_LO;
+    double p = 0x1.6124613a86d09p-33;       /* 1/13! */
+    p = p * r + 0x1.1eed8eff8d898p-29;      /* 1/12! */
+    p = p * r + 0x1.ae64567f544e4p-26;      /* 1/11! */
+    p = p * r + 0x1.27e4fb7789f5cp-22;      /* 1/10! */
+    p = p * r + 0x1.71de3a556c734p-19;      /* 1/9! */
+    p = p * r + 0x1.a01a01a01a01ap-16;      /* 1/8! */
+    p = p * r + 0x1.a01a01a01a01ap-13;      /* 1/7! */
+    p = p * r + 0x1.6c16c16c16c17p-10;      /* 1/6! */
+    p = p * r + 0x1.1111111111111p-7;       /* 1/5! */
+    p = p * r + 0x1.5555555555555p-5;       /* 1/4! */
+    p = p * r + 0x1.5555555555555p-3;       /* 1/3! */
+    p = p * r + 0.5;
+    p = p * r + 1.0;
+    p = p * r + 1.0;
+    if (k >= -1022 && k <= 1023) return p * or_pow2i(k);
+    if (k > 1023) return (p * or_pow2i(1023)) * or_pow2i(k - 1023);
+    return (p * or_pow2i(k + 200)) * or_pow2i(-200);
+}
+
+/* x^y for x > 0, finite y: exp(y log x) with the two functions above */
+double or_det_pow(double x, double y) { return or_det_exp(y * or_det_log(x)); }
+
 /* P:264-265 "weights ... following a power law with exponent beta>2"; R4 fixes the Pareto
  * law P(w >= x) = x^(1-beta), w_min = 1, by inverse transform w = (1-U)^(-1/(beta-1)).
  * U comes from Philox counter (v, 0, 0, 1), words (o0, o1). */
@@ -190,7 +282,7 @@ double or_prob(double wu, double wv, double s, double D, double T)
     double q = (wu * wv) * s;
     double ratio = q / D;
     if (ratio >= 1.0) return 1.0;
-    return pow(ratio, 1.0 / T);
+    return or_det_pow(ratio, 1.0 / T); /* R26 */
 }
 
 /* threshold model P:282-286 in the kappa form of R1: edge iff ||x_u-x_v||^d <= q (inclusive). */
@@ -485,7 +577,7 @@ static void type2(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
             or_philox4x32_10(ctr, c->seed, o);
             c->st->draws++;
             double rj = or_u53(o[0], o[1]), ra = or_u53(o[2], o[3]);
-            double z = pbar == 1.0 ? 0.0 : log(1.0 - rj) / Lbar;
+            double z = pbar == 1.0 ? 0.0 : or_det_log(1.0 - rj) / Lbar; /* R26 */
             int64_t remaining = (int64_t)end - pos - 1;
             /* jump near-tie (R21): floor(z) is an integer decided in double.  glibc's and CUDA's
              * log are each within 1 ulp of log(1-rj), the division is correctly rounded, so the
@@ -630,7 +722,7 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
             or_philox4x32_10(ctr, c->seed, o);
             c->st->draws++;
             double rj = or_u53(o[0], o[1]), ra = or_u53(o[2], o[3]);
-            double z = pbar == 1.0 ? 0.0 : log(1.0 - rj) / Lbar;
+            double z = pbar == 1.0 ? 0.0 : or_det_log(1.0 - rj) / Lbar; /* R26 */
             int64_t remaining = (int64_t)end - pos - 1;
             if ((or_tie_mode & 4) && pbar < 1.0) {
                 double az0 = fabs(z);

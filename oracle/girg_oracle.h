@@ -32,6 +32,11 @@ extern "C" {
 void or_philox4x32_10(const uint32_t ctr[4], uint64_t seed, uint32_t out[4]);
 double or_u53(uint32_t hi, uint32_t lo);
 
+/* ---- R26: canonical log / exp / pow of the edge decisions (+ - * / and bit operations only) ---- */
+double or_det_log(double x);
+double or_det_exp(double t);
+double or_det_pow(double x, double y);
+
 /* ---- model, Sec. 2.1 P:258-290 ---- */
 int or_weights(uint64_t n, double beta, uint64_t seed, double *w);          /* P:264-265, R4 */
 double or_weight_of_uniform(double U, double beta); /* inverse transform (1-U)^(-1/(beta-1)) */

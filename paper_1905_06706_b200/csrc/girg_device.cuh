@@ -5,6 +5,7 @@
 // -fmad=false so every product and sum rounds separately, as in DESIGN.md "Canonical
 // arithmetic").  Citations "P:NNN" refer to lines of PAPER.md (arXiv:1905.06706).
 #pragma once
+#include <math_constants.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -115,6 +116,84 @@ __device__ __forceinline__ void morton_decode(uint32_t code, uint32_t (&c)[D])
 // to right, q = (w_u*w_v)*s, p = min(1, (q/D)^(1/T)) (Eq. 1 P:277 in kappa form), threshold
 // D <= q.
 // ---------------------------------------------------------------------------------------
+// ---------------------------------------------------------------------------------------
+// R26: the log / exp / pow of the edge decisions, written with + - * / and bit
+// operations only (no libdevice), the formulas the oracle states: both sides compute identical
+// bits, so a T > 0 decision cannot differ by a library ulp.  (-fmad=false: no contraction.)
+//   log: x = m 2^k, m in [sqrt(1/2), sqrt(2)), s = (m-1)/(m+1),
+//        log m = 2s (1 + s^2/3 + ... + s^22/23), log x = k ln2_hi + (k ln2_lo + log m)
+//   exp: k = rint(t / ln2), r = (t - k ln2_hi) - k ln2_lo, sum_{i<=13} r^i/i!, times 2^k
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ double pow2i(int k)  // 2^k, -1022 <= k <= 1023
+{
+    return __longlong_as_double((long long)((unsigned long long)(k + 1023) << 52));
+}
+
+__device__ __forceinline__ double det_log(double x)
+{
+    if (!(x > 0.0)) return x == 0.0 ? -CUDART_INF : CUDART_NAN;
+    if (isinf(x)) return x;
+    int k = 0;
+    unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    if (((b >> 52) & 0x7ff) == 0) {
+        x = x * 0x1p54;
+        k = -54;
+        b = (unsigned long long)__double_as_longlong(x);
+    }
+    k += (int)((b >> 52) & 0x7ff) - 1023;
+    double m = __longlong_as_double((long long)((b & 0x000fffffffffffffull) | 0x3ff0000000000000ull));
+    if (m > 0x1.6a09e667f3bcdp+0) {
+        m = m * 0.5;
+        k += 1;
+    }
+    const double f = m - 1.0;
+    const double sv = f / (m + 1.0);
+    const double z = sv * sv;
+    double p = 0x1.642c8590b2164p-5;
+    p = p * z + 0x1.8618618618618p-5;
+    p = p * z + 0x1.af286bca1af28p-5;
+    p = p * z + 0x1.e1e1e1e1e1e1ep-5;
+    p = p * z + 0x1.1111111111111p-4;
+    p = p * z + 0x1.3b13b13b13b14p-4;
+    p = p * z + 0x1.745d1745d1746p-4;
+    p = p * z + 0x1.c71c71c71c71cp-4;
+    p = p * z + 0x1.2492492492492p-3;
+    p = p * z + 0x1.999999999999ap-3;
+    p = p * z + 0x1.5555555555555p-2;
+    const double logm = (2.0 * sv) + (2.0 * sv) * (z * p);
+    const double kd = (double)k;
+    return kd * 0x1.62e42fee00000p-1 + (kd * 0x1.a39ef35793c76p-33 + logm);
+}
+
+__device__ __forceinline__ double det_exp(double t)
+{
+    if (isnan(t)) return t;
+    if (t > 709.78) return CUDART_INF;
+    if (t < -745.2) return 0.0;
+    const double kd = rint(t * 0x1.71547652b82fep+0);
+    const int k = (int)kd;
+    const double r = (t - kd * 0x1.62e42fee00000p-1) - kd * 0x1.a39ef35793c76p-33;
+    double p = 0x1.6124613a86d09p-33;
+    p = p * r + 0x1.1eed8eff8d898p-29;
+    p = p * r + 0x1.ae64567f544e4p-26;
+    p = p * r + 0x1.27e4fb7789f5cp-22;
+    p = p * r + 0x1.71de3a556c734p-19;
+    p = p * r + 0x1.a01a01a01a01ap-16;
+    p = p * r + 0x1.a01a01a01a01ap-13;
+    p = p * r + 0x1.6c16c16c16c17p-10;
+    p = p * r + 0x1.1111111111111p-7;
+    p = p * r + 0x1.5555555555555p-5;
+    p = p * r + 0x1.5555555555555p-3;
+    p = p * r + 0.5;
+    p = p * r + 1.0;
+    p = p * r + 1.0;
+    if (k >= -1022 && k <= 1023) return p * pow2i(k);
+    if (k > 1023) return (p * pow2i(1023)) * pow2i(k - 1023);
+    return (p * pow2i(k + 200)) * pow2i(-200);
+}
+
+__device__ __forceinline__ double det_pow(double x, double y) { return det_exp(y * det_log(x)); }
+
 template <int D>
 __device__ __forceinline__ double dist_pow(const double (&xu)[D], const double (&xv)[D])
 {
@@ -136,7 +215,7 @@ __device__ __forceinline__ double prob_uv(double wu, double wv, double s, double
     const double q = __dmul_rn(__dmul_rn(wu, wv), s);
     const double ratio = __ddiv_rn(q, Dp);
     if (ratio >= 1.0) return 1.0;
-    return pow(ratio, invT);
+    return det_pow(ratio, invT);  // R26
 }
 
 // ---------------------------------------------------------------------------------------

@@ -343,7 +343,7 @@ __device__ __forceinline__ void load_rec(const SampleArgs& a, uint32_t p, double
 
 // ---- cold paths, out of line so that the engine loop stays small in the instruction cache ----
 // canonical jump skip z = log(1-rj)/log1p(-pbar) (R10)
-__device__ __noinline__ double exact_skip(double rj, double Lbar) { return __ddiv_rn(log(__dsub_rn(1.0, rj)), Lbar); }
+__device__ __noinline__ double exact_skip(double rj, double Lbar) { return __ddiv_rn(det_log(__dsub_rn(1.0, rj)), Lbar); }
 // canonical p_uv (Eq. 1, kappa form)
 __device__ __noinline__ double exact_prob(double wu, double wv, double s, double Dp, double invT)
 {

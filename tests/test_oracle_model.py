@@ -382,3 +382,33 @@ def test_geometric_skip(oracle):
     skips = np.array([oracle.geometric_skip(0.3, oracle.u53(*map(int, oracle.philox([k, 1, 0, 9], 1)[:2])))
                       for k in range(50_000)])
     assert abs((skips == 0).mean() - 0.3) < 5 * math.sqrt(0.3 * 0.7 / 50_000)
+
+
+def test_deterministic_log_exp_pow(oracle):
+    """R26: the decisions' log / exp / pow are written with + - * / only (so the CUDA library's
+    independent copy computes the same bits); pinned against the C library: log within 2 ulp,
+    exp within 2 ulp on the normal range, pow within 2e-13 relative on the decisions' range
+    (x in (1e-30, 1), y = 1/T in [1, 50]); exact special values."""
+    import math
+
+    rng = np.random.default_rng(7)
+
+    def ulp(a, b):
+        return abs(int(np.float64(a).view(np.int64)) - int(np.float64(b).view(np.int64)))
+
+    xs = np.concatenate([rng.random(20000), 10.0 ** rng.uniform(-300, 300, 20000),
+                         1 + 1e-10 * rng.standard_normal(2000), [5e-324, 1e-310, 1.7e308, 2.0**-53, 1 - 2.0**-53]])
+    assert max(ulp(oracle.det_log(x), math.log(x)) for x in xs if x > 0) <= 2
+    ts = np.concatenate([rng.uniform(-708, 709, 20000), rng.uniform(-1e-3, 1e-3, 2000)])
+    assert max(ulp(oracle.det_exp(t), math.exp(t)) for t in ts) <= 2
+    worst = 0.0
+    for _ in range(20000):
+        x, y = 10 ** rng.uniform(-30, 0), rng.uniform(1.0, 50.0)
+        e = x**y
+        if e > 1e-300:
+            worst = max(worst, abs(oracle.det_pow(x, y) - e) / e)
+    assert worst < 2e-13
+    assert oracle.det_log(1.0) == 0.0 and oracle.det_exp(0.0) == 1.0
+    assert oracle.det_log(2.0) == pytest.approx(math.log(2.0), rel=1e-16)
+    assert oracle.det_pow(0.3, 1.0) == pytest.approx(0.3, rel=1e-15)
+    assert oracle.det_exp(-800.0) == 0.0 and math.isinf(oracle.det_exp(710.0))
