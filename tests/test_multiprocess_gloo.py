@@ -88,7 +88,7 @@ def test_shard_ranges_partition_blocks():
             assert all(r[0] == sl for r in rs)
             assert rs[0][1] == 0 and rs[-1][2] == 1 << (d * sl)
             assert all(a[2] == b[1] for a, b in zip(rs, rs[1:]))
-            assert (1 << (d * sl)) >= 512 * world or d * (sl + 1) > 30
+            assert (1 << (d * sl)) >= 4096 * world or d * (sl + 1) > 30
 
 
 @pytest.mark.parametrize("scheme", [0, 1])

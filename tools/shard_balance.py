@@ -14,6 +14,7 @@ from paper_1905_06706_b200.sharding import shard_for_rank  # noqa: E402
 from workloads import BY_NAME  # noqa: E402
 
 out = {}
+BPR = int(os.environ.get("GIRG_BLOCKS_PER_RANK", "4096"))
 for name in (sys.argv[1:] or ["C3", "C4", "C5"]):
     c = BY_NAME[name]
     w = girg.weights(c.n, c.beta, c.seed)
@@ -27,8 +28,8 @@ for name in (sys.argv[1:] or ["C3", "C4", "C5"]):
         for mode in ("ranked", "range"):
             ms, es = [], []
             for r in range(world):
-                girg.edges(w, x, c.T, kappa, c.seed, out=buf, shard=shard_for_rank(c.d, world, r, mode=mode))
-                e = girg.edges(w, x, c.T, kappa, c.seed, out=buf, shard=shard_for_rank(c.d, world, r, mode=mode))
+                girg.edges(w, x, c.T, kappa, c.seed, out=buf, shard=shard_for_rank(c.d, world, r, BPR, mode=mode))
+                e = girg.edges(w, x, c.T, kappa, c.seed, out=buf, shard=shard_for_rank(c.d, world, r, BPR, mode=mode))
                 ms.append(girg.last_timings()["ms_sample"])
                 es.append(int(e.shape[0]))
             assert sum(es) == full, (sum(es), full)
