@@ -7,7 +7,7 @@
  * Built with: gcc -O2 -std=c99 -ffp-contract=off -fPIC -shared -lm   (no FMA contraction:
  * the canonical arithmetic of DESIGN.md "Canonical arithmetic" is evaluated literally).
  *
- * Citations "P:NNN" are lines of PAPER.md (arXiv:1905.06706).  Readings R1..R20 are listed
+ * Citations "P:NNN" are lines of PAPER.md (arXiv:1905.06706).  Readings R1..R26 are listed
  * in DESIGN.md; they resolve the places where the paper is silent or garbled.
  */
 #define _GNU_SOURCE

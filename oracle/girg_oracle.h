@@ -8,7 +8,7 @@
  *
  * Plain, sequential, obviously-correct C99 (compiled -O2 -ffp-contract=off, glibc libm).
  * Citations: "P:NNN" = line NNN of /root/reference/PAPER.md (arXiv:1905.06706).
- * Every reading of an ambiguous passage is listed in DESIGN.md ("Readings", R1..R20).
+ * Every reading of an ambiguous passage is listed in DESIGN.md ("Readings", R1..R26).
  *
  * Parity status of every function is pinned by tests/test_oracle_*.py; see DESIGN.md
  * section "Oracle pins".  No function here is "parity unpinned".

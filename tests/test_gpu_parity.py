@@ -367,7 +367,7 @@ def test_crowded_cell_linear_order(d, T, nc, kappa):
 
 
 @pytest.mark.parametrize("d,T,scheme", [(2, 0.8, girg.SCHEME_MERGED), (3, 0.9, girg.SCHEME_MERGED),
-                                        (1, 0.5, girg.SCHEME_EVENT)])
+                                        (1, 0.5, girg.SCHEME_EVENT), (2, 0.0, girg.SCHEME_MERGED)])
 def test_ranked_shards_equal_oracle_and_union(d, T, scheme):
     """Interleaved multi-GPU ownership (girg_options.nranks, sharding.shard_for_rank): every rank's
     shard equals the oracle's shard of the same rank, and the N shards partition the full graph."""
@@ -388,3 +388,18 @@ def test_ranked_shards_equal_oracle_and_union(d, T, scheme):
         assert np.array_equal(g, O.sort_edges(eo)), r
         parts.append(g)
     assert np.array_equal(np.sort(np.concatenate(parts)), full)
+
+
+def test_batch_binomial_d3_many_graphs_and_overflowing_capacity():
+    """Fused batch at T > 0, d = 3 with more graphs than one block row per SM and two graphs whose
+    capacity is too small: every graph equals its single call, the small ones report their count."""
+    n, d, T, beta, B = 4000, 3, 0.9, 2.9, 40
+    ws = [girg.weights(n, beta, 500 + g) for g in range(B)]
+    xs = [girg.positions(n, d, 900 + g) for g in range(B)]
+    kap = [girg.scale_weights(w, 12.0, d, T, beta) for w in ws]
+    seeds = [77 + g for g in range(B)]
+    caps = [16 * n] * B
+    caps[5] = caps[31] = 3
+    out = girg.edges_batch(ws, xs, T, kap, seeds, caps=caps)
+    for g in range(B):
+        assert np.array_equal(gpu_keys(out[g]), gpu_keys(girg.edges(ws[g], xs[g], T, kap[g], seeds[g]))), g
