@@ -45,6 +45,16 @@
 #endif
 
 constexpr int SCHEME_EVENT = 0, SCHEME_MERGED = 1;
+// Unrolling of the job setup's shared-memory loops (runtime trip counts; nvcc unrolls them 4x by
+// default).  The sampling kernels are instruction-fetch bound as much as issue bound (ncu C5:
+// no_instructions is the top stall reason, the hot code is ~33 KB against a 32 KB L1.5 I$), so
+// the setup loops stay rolled: fewer code bytes at a few more instructions per job.
+#ifndef GIRG_SETUP_UNROLL
+#define GIRG_SETUP_UNROLL 1
+#endif
+#define GIRG_STR2(x) #x
+#define GIRG_STR(x) GIRG_STR2(x)
+#define SETUP_LOOP _Pragma(GIRG_STR(unroll GIRG_SETUP_UNROLL))
 #ifndef GIRG_EB
 #define GIRG_EB 128
 #endif
@@ -452,6 +462,7 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
         uint32_t pc[D];
         morton_decode<D>(t.Cpar, pc);
         const uint32_t mask = (1u << t.lg) - 1u;
+        SETUP_LOOP
         for (int q = lane; q < t.npar; q += 32) {
             uint32_t c[D];
             int r = q;
@@ -471,8 +482,10 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
             const int q = lane + 32 * s;
             rk[s] = 0;
             mine[s] = q < t.npar ? S.par[q] : 0u;
-            if (q < t.npar)
+            if (q < t.npar) {
+                SETUP_LOOP
                 for (int o = 0; o < t.npar; ++o) rk[s] += S.par[o] < mine[s];
+            }
         }
         __syncwarp();
 #pragma unroll
@@ -565,6 +578,7 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
         if (t.l >= 1) {  // sub-cells = the 2^d children of each region parent: separable per dimension
             uint32_t cpc[D];  // coordinates of the task cell (level l-1)
             morton_decode<D>(t.Cpar, cpc);
+            SETUP_LOOP
             for (int idx = lane; idx < nc * t.npar; idx += 32) {
                 const int cc = idx / t.npar, q = idx - cc * t.npar;
                 const int e = S.child[cc];
@@ -728,6 +742,7 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
         if (q3 < nc * 3) {
             const int cc = q3 / 3, k = q3 - 3 * cc;
             uint32_t acc = 0;
+            SETUP_LOOP
             for (int q = 0; q < t.npar; ++q) {
                 const uint32_t c = S.pre[cc][k][q];
                 S.pre[cc][k][q] = acc;
@@ -796,6 +811,7 @@ __device__ __noinline__ JobSetup setup_job1(const SampleArgs& a, Slot1& S, const
         int nk[3] = {0, 0, 0};
         const bool near = t.lg >= 2;  // l = lg + G >= 6: offsets -3..3 are distinct and inside the region
         const int ncand = near ? 7 : t.npar * nsub;
+        SETUP_LOOP
         for (int c = 0; c < ncand; ++c) {
             uint32_t B;
             int q, kk;
@@ -1088,10 +1104,13 @@ struct TileSource {
         start = warp_excl_scan(cnt, total);
         tk = 0;
         // prefetch the tile's first 32 task entries, one per lane (their loads overlap the jobs)
+        // owner of task entry `lane`: the last point whose start <= lane (starts are an exclusive
+        // scan, so for lane < total this is the nonempty list holding it); binary search
         int owner = 0;
-        for (int src = 0; src < 32; ++src) {
-            const uint32_t sc = __shfl_sync(FULL, cnt, src), ss = __shfl_sync(FULL, start, src);
-            if (sc > 0 && ss <= lane) owner = src;
+#pragma unroll
+        for (int step = 16; step; step >>= 1) {
+            const uint32_t ss = __shfl_sync(FULL, start, owner + step < 32 ? owner + step : 31);
+            if (owner + step < 32 && ss <= lane) owner += step;
         }
         const uint32_t otoff = __shfl_sync(FULL, toffv, owner), ostart = __shfl_sync(FULL, start, owner);
         task32 = lane < total ? __ldg(&a.tasks[otoff + (lane - ostart)]) : (uint16_t)0;
@@ -1252,6 +1271,11 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         int nk = -1;
         uint32_t npa = 0, npb = 0;
         double nra = 0.0, npbar = 1.0;
+        // the lane's one lookup of this iteration (its landing or a dispatched type-I candidate):
+        // slot << 8 | child << 2 | kind (-1: none) and the index in the sequence's row-major space,
+        // resolved by a single divmod + locate below (one code copy, executed by both lane kinds)
+        int lpack = -1;
+        unsigned long long lval = 0;
         if (chain) {
             const SlotT<D>& S = W.slot[ls];
             const Seq& Q = S.seq[cc][kind];
@@ -1285,19 +1309,8 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 nk = kind;
                 nra = u53(o.z, o.w);
                 npbar = pb_;
-                const unsigned long long g = (unsigned long long)pos;
-                if (SCHEME == SCHEME_MERGED) {
-                    uint32_t ti;
-                    const uint32_t si = divmod(g, Q.M, ti);
-                    uint32_t B;
-                    npa = Q.a0 + si;
-                    npb = locate(S, S.job.npar, S.job.cs, cc, kind, ti, B);
-                } else {
-                    uint32_t ti;
-                    const uint32_t si = divmod(g, enB, ti);
-                    npa = Q.a0 + si;
-                    npb = eb0 + ti;
-                }
+                lpack = (ls << 8) | (cc << 2) | kind;
+                lval = (unsigned long long)pos;
             }
         }
         // ---- (3) evaluate the pending candidate (records loaded last iteration) ----
@@ -1369,12 +1382,8 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 const Seq& Q = S.seq[qc][qk];
                 const unsigned long long x = u - S.uoff[q];
                 if (qk == 0) {
-                    uint32_t ti;
-                    const uint32_t si = divmod(x, Q.M, ti);
-                    uint32_t B;
-                    npa = Q.a0 + si;
-                    npb = locate(S, S.job.npar, S.job.cs, qc, 0, ti, B);
-                    if (!(S.job.same_layer && B == Q.A && npb <= npa)) nk = 0;  // same cell: only s < t (R16)
+                    lpack = (ds << 8) | (qc << 2);
+                    lval = x;
                 } else {
                     chain = true;
                     ls = ds;
@@ -1403,6 +1412,23 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
             dnext = min(dhi, dnext + __popc(idle));
             if (dnext < dhi)
                 while (dq < 3 * Geo<D>::CB - 1 && W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
+        }
+        // ---- the lookup: row-major index -> (row s, column t) -> sorted positions ----
+        if (lpack >= 0) {
+            const int lk = lpack & 3, lc = (lpack >> 2) & 63;
+            const SlotT<D>& S = W.slot[lpack >> 8];
+            const Seq& Q = S.seq[lc][lk];
+            const bool ev = SCHEME == SCHEME_EVENT && lk > 0;  // EVENT landing: one cell (enB, eb0)
+            uint32_t ti;
+            const uint32_t si = divmod(lval, ev ? enB : Q.M, ti);
+            npa = Q.a0 + si;
+            if (ev) {
+                npb = eb0 + ti;
+            } else {
+                uint32_t B;
+                npb = locate(S, S.job.npar, S.job.cs, lc, lk, ti, B);
+                if (lk == 0 && !(S.job.same_layer && B == Q.A && npb <= npa)) nk = 0;  // same cell: only s < t (R16)
+            }
         }
         // ---- (5) issue the loads of the next candidate ----
         pk = nk;

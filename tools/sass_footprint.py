@@ -45,3 +45,21 @@ for i, x in enumerate(xs):
         print(f"  {marks[0] * 100:.1f}% of executed instructions covered by {i + 1} instructions = {16 * (i + 1) / 1024:.1f} KB")
         marks.pop(0)
 print("executed-once-or-more instructions:", sum(1 for x in xs if x > 0), f"= {16 * sum(1 for x in xs if x > 0) / 1024:.0f} KB")
+
+if len(sys.argv) > 2:  # per source line: SASS instructions in the hot set (covering 99 %) and executions
+    thr = None
+    acc = 0
+    for x in xs:
+        acc += x
+        if acc >= 0.99 * tot:
+            thr = x
+            break
+    per = defaultdict(lambda: [0, 0])
+    for ex, line, _ in sass.values():
+        if ex >= thr:
+            per[line][0] += 1
+            per[line][1] += ex
+    rows = sorted(per.items(), key=lambda kv: -kv[1][0])
+    print(f"hot set (executions >= {thr}): {sum(v[0] for v in per.values())} SASS instructions")
+    for line, (n, ex) in rows[: int(sys.argv[2])]:
+        print(f"{n:5d} instr {ex / tot * 100:5.1f}% exec  {line}")
