@@ -307,7 +307,8 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t v, uint32_t& total)
     return x - v;
 }
 
-__device__ __forceinline__ void warp_flush(const SampleArgs& a, uint2* buf, unsigned& fill)
+// write the warp's staged edges (out of line: once per ~EB edges, keeps the engine loop small)
+__device__ __noinline__ void warp_flush_n(const SampleArgs& a, const uint2* buf, unsigned fill)
 {
     __syncwarp();
     unsigned long long base = 0;
@@ -318,6 +319,26 @@ __device__ __forceinline__ void warp_flush(const SampleArgs& a, uint2* buf, unsi
         if (slot < a.cap) a.edges[slot] = buf[k];
     }
     __syncwarp();
+}
+
+#ifndef GIRG_FLUSH_CALL
+#define GIRG_FLUSH_CALL 0  // 1: out-of-line flush (C4 -1 %, but C3 +6 %, C5 +0.5 %: the call perturbs the 64-register d = 2 engine)
+#endif
+__device__ __forceinline__ void warp_flush(const SampleArgs& a, uint2* buf, unsigned& fill)
+{
+#if GIRG_FLUSH_CALL
+    warp_flush_n(a, buf, fill);
+#else
+    __syncwarp();
+    unsigned long long base = 0;
+    if (lane_id() == 0 && fill) base = atomicAdd(a.m, (unsigned long long)fill);
+    base = shfl64(base, 0);
+    for (unsigned k = lane_id(); k < fill; k += 32) {
+        const unsigned long long slot = base + k;
+        if (slot < a.cap) a.edges[slot] = buf[k];
+    }
+    __syncwarp();
+#endif
     fill = 0;
 }
 
@@ -423,7 +444,7 @@ struct JobSetup {
 // (l < sl, which would all fall to a few first-descendant blocks) rank = (A + 7 j + 13 i + 31 l)
 // mod nranks, spreading them by identity.
 template <int D>
-__device__ __forceinline__ bool owns(const SampleArgs& a, uint32_t A, int l, int i, int j)
+__device__ __noinline__ bool owns(const SampleArgs& a, uint32_t A, int l, int i, int j)
 {
     if (a.nranks == 0) {
         const unsigned long long b = l >= a.sl ? ((unsigned long long)A >> (D * (l - a.sl)))
@@ -527,7 +548,7 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
             if (e < nsub) {
                 ok = S.achild[e + 1] > S.achild[e];
                 const uint32_t A = (t.Cpar << t.cs) + (uint32_t)e;
-ok = ok && owns<D>(a, A, t.l, t.i, t.j);
+                ok = ok && (!a.sharded || owns<D>(a, A, t.l, t.i, t.j));
             }
             const unsigned bm = __ballot_sync(FULL, ok);
             const int rank = cnt + __popc(bm & ((1u << lane) - 1u));
@@ -1027,7 +1048,7 @@ __device__ __forceinline__ void flush_counters(const SampleArgs& a, const Counte
 }
 
 // queue a job's unit range as items of ~ITEM_WORK weighted units (lane 0)
-__device__ __forceinline__ void push_items(const SampleArgs& a, const TaskDesc& t, uint16_t task, int batch,
+__device__ __noinline__ void push_items(const SampleArgs& a, const TaskDesc& t, uint16_t task, int batch,
                                            unsigned long long U, unsigned long long work)
 {
     if (lane_id() == 0) {
@@ -1365,7 +1386,8 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                     dnext = lo;
                     dhi = hi;
                     dq = 0;
-                    while (dq < 3 * Geo<D>::CB - 1 && W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
+#pragma unroll 1
+                while (dq < 3 * Geo<D>::CB - 1 && W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
                 } else {
                     more = false;
                 }
@@ -1377,6 +1399,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
             if (u < dhi) {
                 const SlotT<D>& S = W.slot[ds];
                 int q = dq;  // sequence holding unit u
+#pragma unroll 1
                 while (q < 3 * Geo<D>::CB - 1 && S.uoff[q + 1] <= u) ++q;
                 const int qc = q / 3, qk = q - 3 * qc;
                 const Seq& Q = S.seq[qc][qk];
@@ -1411,6 +1434,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         if (dnext < dhi) {
             dnext = min(dhi, dnext + __popc(idle));
             if (dnext < dhi)
+#pragma unroll 1
                 while (dq < 3 * Geo<D>::CB - 1 && W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
         }
         // ---- the lookup: row-major index -> (row s, column t) -> sorted positions ----
@@ -1494,6 +1518,7 @@ __device__ __forceinline__ void engine_cand(const SampleArgs& a, WarpSmem<D>& W,
             uint32_t ua = 0, ub = 0;
             if (u < hi) {
                 int q = 0;
+#pragma unroll 1
                 while (q < 3 * Geo<D>::CB - 1 && S.uoff[q + 1] <= u) ++q;
                 const int qc = q / 3;
                 const Seq& Q = S.seq[qc][0];
