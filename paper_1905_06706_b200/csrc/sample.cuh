@@ -1079,6 +1079,10 @@ __device__ __noinline__ void push_items(const SampleArgs& a, const TaskDesc& t, 
 // k_sample: persistent warps pull tiles of 32 sorted points; each point lists the jobs it owns
 template <int D, int SCHEME, bool STATS>
 struct TileSource {
+    // the engine resolves a lane's landing / type-I lookup at one code site (k_sample: 137.6 ->
+    // 117.7 ms on C5); k_big keeps them in place, where the merged site's longer-lived 64-bit
+    // index made the chain state spill (36.5 -> 42.8 ms)
+    static constexpr bool unified_lookup = true;
     unsigned tile = 0;
     uint32_t total = 0, tk = 0;  // jobs of the tile (warp-uniform), next one
     int i = 0, lf = 255;         // this lane's point
@@ -1197,6 +1201,7 @@ struct TileSource {
 // k_big: warps pull queued items (unit ranges of big jobs)
 template <int D, int SCHEME, bool STATS>
 struct ItemSource {
+    static constexpr bool unified_lookup = false;  // see TileSource
     unsigned nit;
     __device__ __noinline__ bool next(const SampleArgs& a, SlotT<D>& S, unsigned long long& lo,
                                          unsigned long long& hi, Counters& C)
@@ -1330,8 +1335,21 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 nk = kind;
                 nra = u53(o.z, o.w);
                 npbar = pb_;
-                lpack = (ls << 8) | (cc << 2) | kind;
-                lval = (unsigned long long)pos;
+                if constexpr (Src::unified_lookup) {
+                    lpack = (ls << 8) | (cc << 2) | kind;
+                    lval = (unsigned long long)pos;
+                } else {
+                    const unsigned long long g = (unsigned long long)pos;
+                    uint32_t ti;
+                    const uint32_t si = divmod(g, SCHEME == SCHEME_MERGED ? Q.M : enB, ti);
+                    npa = Q.a0 + si;
+                    if (SCHEME == SCHEME_MERGED) {
+                        uint32_t B;
+                        npb = locate(S, S.job.npar, S.job.cs, cc, kind, ti, B);
+                    } else {
+                        npb = eb0 + ti;
+                    }
+                }
             }
         }
         // ---- (3) evaluate the pending candidate (records loaded last iteration) ----
@@ -1405,8 +1423,17 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 const Seq& Q = S.seq[qc][qk];
                 const unsigned long long x = u - S.uoff[q];
                 if (qk == 0) {
-                    lpack = (ds << 8) | (qc << 2);
-                    lval = x;
+                    if constexpr (Src::unified_lookup) {
+                        lpack = (ds << 8) | (qc << 2);
+                        lval = x;
+                    } else {
+                        uint32_t ti;
+                        const uint32_t si = divmod(x, Q.M, ti);
+                        uint32_t B;
+                        npa = Q.a0 + si;
+                        npb = locate(S, S.job.npar, S.job.cs, qc, 0, ti, B);
+                        if (!(S.job.same_layer && B == Q.A && npb <= npa)) nk = 0;  // same cell: only s < t (R16)
+                    }
                 } else {
                     chain = true;
                     ls = ds;
@@ -1438,7 +1465,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 while (dq < 3 * Geo<D>::CB - 1 && W.slot[ds].uoff[dq + 1] <= dnext) ++dq;
         }
         // ---- the lookup: row-major index -> (row s, column t) -> sorted positions ----
-        if (lpack >= 0) {
+        if (Src::unified_lookup && lpack >= 0) {
             const int lk = lpack & 3, lc = (lpack >> 2) & 63;
             const SlotT<D>& S = W.slot[lpack >> 8];
             const Seq& Q = S.seq[lc][lk];
