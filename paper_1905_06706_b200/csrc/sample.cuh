@@ -54,7 +54,11 @@ constexpr int SCHEME_EVENT = 0, SCHEME_MERGED = 1;
 #endif
 #define GIRG_STR2(x) #x
 #define GIRG_STR(x) GIRG_STR2(x)
+#if GIRG_SETUP_UNROLL > 0
 #define SETUP_LOOP _Pragma(GIRG_STR(unroll GIRG_SETUP_UNROLL))
+#else
+#define SETUP_LOOP  // nvcc's default unrolling
+#endif
 #ifndef GIRG_EB
 #define GIRG_EB 128
 #endif
@@ -124,6 +128,9 @@ constexpr unsigned FULL = 0xffffffffu;
 #ifndef GIRG_MINB3
 #define GIRG_MINB3 5
 #endif
+#ifndef GIRG_MINB3_BIG
+#define GIRG_MINB3_BIG GIRG_MINB3
+#endif
 template <int D>
 struct Geo {
     static constexpr int G = D == 1 ? GIRG_G1 : (D == 2 ? GIRG_G2 : 1);  // levels between a task cell and its children
@@ -133,6 +140,7 @@ struct Geo {
     static constexpr int CB = D <= 2 ? NCH : (D == 3 ? GIRG_CB3 : (D == 4 ? 4 : 2));  // children per job (batch)
     static constexpr int WPB = D == 1 ? GIRG_WPB1 : (D == 2 ? 8 : (D == 3 ? GIRG_WPB3 : 2));  // warps per block
     static constexpr int MINB = D == 1 ? GIRG_MINB1 : (D == 2 ? GIRG_MINB2 : (D == 3 ? GIRG_MINB3 : 1));  // resident blocks per SM
+    static constexpr int MINB_BIG = D == 3 ? GIRG_MINB3_BIG : MINB;  // the same for k_big (its own register budget)
     static constexpr int EB = D == 3 ? GIRG_EB3 : GIRG_EB;  // staged edges per warp (d = 3: small, so 5 blocks fit)
     static constexpr int NSLOT = D == 1 ? GIRG_NSLOT1 : (D == 2 ? GIRG_NSLOT2 : (D == 3 ? GIRG_NSLOT3 : 2));  // job slots per warp
     static constexpr int RECW = D == 1 ? 2 : (D <= 3 ? 4 : 6);       // doubles per point record
@@ -325,6 +333,9 @@ __device__ __noinline__ void warp_flush_n(const SampleArgs& a, const uint2* buf,
 // the divergent walk over the mask bits (0); C5 sampling 156.9 -> 150.2 ms, C3 9.56 -> 9.33
 #ifndef GIRG_LOCATE_PRED
 #define GIRG_LOCATE_PRED 1
+#endif
+#ifndef GIRG_T0_ROLL
+#define GIRG_T0_ROLL 0  // the flat T = 0 loop keeps its per-candidate sequence scan unrolled (rolled: n = 2^24 d = 1 10.9 -> 14.1 ms)
 #endif
 #ifndef GIRG_FLUSH_CALL
 #define GIRG_FLUSH_CALL 0  // 1: out-of-line flush (C4 -1 %, but C3 +6 %, C5 +0.5 %: the call perturbs the 64-register d = 2 engine)
@@ -1571,7 +1582,9 @@ __device__ __forceinline__ void engine_cand(const SampleArgs& a, WarpSmem<D>& W,
             uint32_t ua = 0, ub = 0;
             if (u < hi) {
                 int q = 0;
+#if GIRG_T0_ROLL
 #pragma unroll 1
+#endif
                 while (q < 3 * Geo<D>::CB - 1 && S.uoff[q + 1] <= u) ++q;
                 const int qc = q / 3;
                 const Seq& Q = S.seq[qc][0];
@@ -1625,7 +1638,7 @@ __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_sample_t0(Sa
 }
 
 template <int D, bool STATS>
-__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_big_t0(SampleArgs a)
+__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB_BIG) k_big_t0(SampleArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
@@ -1637,7 +1650,7 @@ __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_big_t0(Sampl
 }
 
 template <int D, int SCHEME, bool STATS>
-__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_big(SampleArgs a)
+__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB_BIG) k_big(SampleArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
@@ -1667,7 +1680,7 @@ __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_sample_b(con
 }
 
 template <int D, int SCHEME, bool STATS>
-__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_big_b(const SampleArgs* __restrict__ args)
+__global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB_BIG) k_big_b(const SampleArgs* __restrict__ args)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ SampleArgs sa;

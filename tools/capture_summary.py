@@ -48,7 +48,7 @@ def main():
     p = os.path.join(ROOT, "profiles", "ncu_issue.json")
     t = json.load(open(p)) if os.path.exists(p) else {}
     t["_note"] = ("issue-slot evidence of the sampling kernels (ncu --set full --clock-control none, one launch each, "
-                  "python tools/prof_one.py CFG merged 1 nostats); raw pages in profiles/r02/; consumed by bench.py as "
+                  "python tools/prof_one.py CFG merged 1 nostats); raw pages in profiles/r02/final/; consumed by bench.py as "
                   "roofline.issue; written by tools/capture_summary.py")
     t[cfg] = {"k_sample": s, "k_big": b, "sampling_phase": {
         "warp_inst": wi, "warp_inst_per_edge": wi / m,

@@ -5,20 +5,21 @@ import csv
 import gzip
 import sys
 
-REGIONS = [  # (file, lo, hi, name)
-    ("sample.cuh", 296, 322, "emit/flush"),
-    ("sample.cuh", 323, 338, "load_rec"),
-    ("sample.cuh", 341, 377, "divmod/chunk_log2/exact"),
-    ("sample.cuh", 378, 518, "setup_common (region, ranges, children)"),
-    ("sample.cuh", 519, 872, "setup_job (classify, prefixes, offsets)"),
-    ("sample.cuh", 873, 967, "locate"),
-    ("sample.cuh", 968, 1010, "counters/push_items"),
-    ("sample.cuh", 1011, 1162, "tile/item source"),
-    ("sample.cuh", 1163, 1500, "engine loop"),
+REGIONS = [  # (file, lo, hi, name): sample.cuh / girg_device.cuh as of the final round-2 code
+    ("sample.cuh", 280, 366, "warp helpers, emit/flush"),
+    ("sample.cuh", 367, 383, "load_rec"),
+    ("sample.cuh", 384, 437, "divmod/chunk_log2/exact"),
+    ("sample.cuh", 438, 589, "setup_common (region, ranges, children)"),
+    ("sample.cuh", 590, 939, "setup_job (classify, prefixes, offsets)"),
+    ("sample.cuh", 940, 1061, "locate"),
+    ("sample.cuh", 1062, 1105, "counters/push_items"),
+    ("sample.cuh", 1106, 1266, "tile/item source"),
+    ("sample.cuh", 1267, 1700, "engine loop"),
     ("girg_device.cuh", 1, 40, "philox/u53"),
-    ("girg_device.cuh", 41, 115, "morton"),
-    ("girg_device.cuh", 116, 140, "dist/prob"),
-    ("girg_device.cuh", 141, 400, "fast paths"),
+    ("girg_device.cuh", 41, 119, "morton"),
+    ("girg_device.cuh", 120, 196, "det_log/exp (R26, exact paths)"),
+    ("girg_device.cuh", 197, 226, "dist/prob"),
+    ("girg_device.cuh", 227, 400, "fast paths"),
 ]
 
 

@@ -13,7 +13,7 @@ timeout 300 python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/
     --log-file gpurun_out/ev3_launches_c5.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/ev3_ncu_launch.log 2>&1
 for c in C5 C4; do
   for k in k_sample k_big; do
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:"^$k<" -c 1 -o /tmp/ev3_${c}_${k} -f \
+    timeout 900 ncu --set full --clock-control none --import-source on -k $k -c 1 -o /tmp/ev3_${c}_${k} -f \
       python tools/prof_one.py $c merged 1 nostats > gpurun_out/ev3_ncu_${c}_${k}.log 2>&1
     ncu -i /tmp/ev3_${c}_${k}.ncu-rep --page raw --csv > gpurun_out/ev3_raw_${c}_${k}.csv 2>&1
     ncu -i /tmp/ev3_${c}_${k}.ncu-rep --page source --csv --print-source cuda,sass > /tmp/ev3_src_${c}_${k}.csv 2>&1
