@@ -189,6 +189,7 @@ struct SampleArgs {
     const uint32_t* sid;
     const uint32_t* P;
     uint32_t n, ntiles;
+    uint32_t tile_pts;  // sorted points per tile (32; fewer for small graphs: more warps in flight)
     uint32_t k0, k1;
     uint2* edges;
     unsigned long long cap;
@@ -1141,11 +1142,11 @@ struct TileSource {
         if (lane == 0) t = atomicAdd(a.tile_ctr, 1u);
         tile = __shfl_sync(FULL, t, 0);
         if (tile >= a.ntiles) return false;
-        const uint32_t p = tile * 32 + lane;
+        const uint32_t p = tile * a.tile_pts + lane;
         i = 0;
         lf = 255;
         code = 0;
-        if (p < a.n) {
+        if (lane < a.tile_pts && p < a.n) {
             int lo = 0, hi = pl->L - 1;  // layer: last with lstart <= p
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
