@@ -1446,7 +1446,10 @@ __global__ void __launch_bounds__(SC_THREADS) k_scale(const double* __restrict__
             }
         } else {
             const uint32_t k = atomicAdd(&ctl->ncand, 1u);
-            if (k < cap) cand[k] = wv;
+            if (k < cap) {
+                cand[k] = wv;
+                cand[cap + k] = invT > 0.0 ? pow(wv / wmax, invT) : 0.0;  // zeta (the host search's power terms)
+            }
         }
     }
     for (int o = 16; o; o >>= 1) {
@@ -1477,13 +1480,13 @@ struct LazyEstimator {
     double T, W, wmax, tau;
     TailSums tail;
     std::vector<double> C;  // candidates: C[0, L) sorted decreasing, C[L, end) unsorted and < C[L-1]
+    std::vector<double> Z;  // their zeta = (c / wmax)^(1/T), computed by the device pass, permuted with C
     size_t L = 0;
     std::vector<double> zeta, suf1, suf2, sufz1, sufz2;  // over C[0, L): zeta and suffix sums (from k to L)
     std::vector<double> pre1, prez;                      // prefix sums of C and zeta over C[0, L)
     double r1 = 0, r2 = 0, rz1 = 0, rz2 = 0;             // sums over the unsorted rest
     double rest_max = 0;                                 // largest unsorted candidate
 
-    double zf(double c) const { return T > 0.0 ? std::pow(c / wmax, 1.0 / T) : 0.0; }
     void reset()
     {
         L = 0;
@@ -1501,7 +1504,7 @@ struct LazyEstimator {
         r1 = r2 = rz1 = rz2 = 0.0;
         rest_max = 0.0;
         for (size_t k = L; k < C.size(); ++k) {
-            const double z = zf(C[k]);
+            const double z = Z[k];
             r1 += C[k];
             r2 += C[k] * C[k];
             rz1 += z;
@@ -1514,12 +1517,20 @@ struct LazyEstimator {
     void cover(double t)
     {
         if (L == C.size() || !(rest_max > t)) return;
-        auto mid = std::partition(C.begin() + L, C.end(), [t](double c) { return c > t; });
-        const size_t L2 = (size_t)(mid - C.begin());
-        std::sort(C.begin() + L, C.begin() + L2, [](double x, double y) { return x > y; });
+        std::vector<std::pair<double, double>> cz(C.size() - L);
+        for (size_t k = L; k < C.size(); ++k) cz[k - L] = {C[k], Z[k]};
+        auto mid = std::partition(cz.begin(), cz.end(), [t](const std::pair<double, double>& c) { return c.first > t; });
+        std::sort(cz.begin(), mid, [](const std::pair<double, double>& x, const std::pair<double, double>& y) {
+            return x.first > y.first;
+        });
+        for (size_t k = L; k < C.size(); ++k) {
+            C[k] = cz[k - L].first;
+            Z[k] = cz[k - L].second;
+        }
+        const size_t L2 = L + (size_t)(mid - cz.begin());
+        zeta.resize(L2);
+        for (size_t k = L; k < L2; ++k) zeta[k] = Z[k];
         L = L2;
-        zeta.resize(L);
-        for (size_t k = 0; k < L; ++k) zeta[k] = zf(C[k]);
         suf1.assign(L + 1, 0.0);
         suf2.assign(L + 1, 0.0);
         sufz1.assign(L + 1, 0.0);
@@ -1591,10 +1602,11 @@ static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double
         for (int attempt = 0; attempt < 24; ++attempt) {
             // ---- device pass ----
             {
+                const auto tp0 = std::chrono::steady_clock::now();
                 Scratch S(st);
                 const size_t o1 = Scratch::rounded(sizeof(ScaleCtl)), o2 = o1 + Scratch::rounded(nb * sizeof(Acc192)),
                              o3 = o2 + Scratch::rounded(nb * sizeof(TailSums));
-                char* blk = S.alloc<char>(o3 + (size_t)cap * sizeof(double));
+                char* blk = S.alloc<char>(o3 + 2 * (size_t)cap * sizeof(double));  // candidates, then their zeta
                 ScaleCtl* ctl = (ScaleCtl*)blk;
                 Acc192* wpart = (Acc192*)(blk + o1);
                 TailSums* tpart = (TailSums*)(blk + o2);
@@ -1624,10 +1636,14 @@ static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double
                 E.tau = out.tau;
                 E.tail = out.tail;
                 E.C.resize(out.ncand);
+                E.Z.resize(out.ncand);
                 if (out.ncand) {
                     GCHECK(cudaMemcpyAsync(E.C.data(), cand, out.ncand * sizeof(double), cudaMemcpyDeviceToHost, st));
+                    GCHECK(cudaMemcpyAsync(E.Z.data(), cand + cap, out.ncand * sizeof(double), cudaMemcpyDeviceToHost,
+                                           st));
                     GCHECK(cudaStreamSynchronize(st));
                 }
+                const auto tp1 = std::chrono::steady_clock::now();
                 E.reset();
                 // ---- host search (exponential bracket, bisection in log kappa, R12) ----
                 const double k0 = out.kappa0;
@@ -1689,9 +1705,13 @@ static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double
                     }
                 }
                 static const bool dbg = getenv("GIRG_SCALE_DEBUG") != nullptr;
-                if (dbg)
-                    fprintf(stderr, "[girg scale] attempt %d ncand %u sorted %zu tau %g ok %d iters %d kappa0 %g\n",
-                            attempt, out.ncand, E.L, E.tau, (int)ok, it, k0);
+                if (dbg) {
+                    const auto tp2 = std::chrono::steady_clock::now();
+                    fprintf(stderr, "[girg scale] attempt %d ncand %u sorted %zu tau %g ok %d iters %d kappa0 %g device+copy %.3f ms search %.3f ms\n",
+                            attempt, out.ncand, E.L, E.tau, (int)ok, it, k0,
+                            std::chrono::duration<double, std::milli>(tp1 - tp0).count(),
+                            std::chrono::duration<double, std::milli>(tp2 - tp1).count());
+                }
                 if (ok) {
                     *kappa_out = 0.5 * (lo + hi);
                     return GIRG_OK;
