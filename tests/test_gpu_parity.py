@@ -403,3 +403,22 @@ def test_batch_binomial_d3_many_graphs_and_overflowing_capacity():
     out = girg.edges_batch(ws, xs, T, kap, seeds, caps=caps)
     for g in range(B):
         assert np.array_equal(gpu_keys(out[g]), gpu_keys(girg.edges(ws[g], xs[g], T, kap[g], seeds[g]))), g
+
+
+@pytest.mark.parametrize("d,T", [(1, 0.0), (2, 0.7), (3, 0.9)])
+def test_edge_set_independent_of_tile_size(d, T, monkeypatch):
+    """The sampler's schedule (sorted points per tile: 8 below 2^17 points, else 32; any 1..32 by
+    GIRG_TILE_PTS) does not change the edge set -- the randomness is keyed by vertex pair and
+    cell-pair chunk (R17, R22), not by warp or lane -- and equals the oracle's."""
+    n, beta, seed = 40_000, 2.5, 31 + d
+    w, x = synth_inputs(n, d, beta, seed)
+    kappa = O.scale_weights(w, 10.0, d, T, beta)
+    eo = O.sort_edges(O.edges(w, x, d, T, kappa, seed))
+    wd, xd = dev(w), dev(x)
+    for tp in (None, "32", "13", "4", "1"):
+        if tp is None:
+            monkeypatch.delenv("GIRG_TILE_PTS", raising=False)
+        else:
+            monkeypatch.setenv("GIRG_TILE_PTS", tp)
+        g = gpu_keys(girg.edges(wd, xd, T, kappa, seed))
+        assert np.array_equal(g, eo), (tp, len(g), len(eo))
