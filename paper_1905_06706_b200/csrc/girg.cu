@@ -1489,15 +1489,68 @@ struct LazyEstimator {
 
     void reset()
     {
-        L = 0;
-        zeta.clear();
-        pre1.assign(1, 0.0);
-        prez.assign(1, 0.0);
-        suf1.assign(1, 0.0);
-        suf2.assign(1, 0.0);
-        sufz1.assign(1, 0.0);
-        sufz2.assign(1, 0.0);
+        // all candidates sorted once (radix_desc: a few linear passes, no comparison sort of the
+        // growing prefix), so cover() below has nothing left to do
+        radix_desc(C, Z);
+        L = C.size();
+        zeta = Z;
+        suf1.assign(L + 1, 0.0);
+        suf2.assign(L + 1, 0.0);
+        sufz1.assign(L + 1, 0.0);
+        sufz2.assign(L + 1, 0.0);
+        for (size_t k = L; k-- > 0;) {  // ascending weights: small terms first
+            suf1[k] = suf1[k + 1] + C[k];
+            suf2[k] = suf2[k + 1] + C[k] * C[k];
+            sufz1[k] = sufz1[k + 1] + zeta[k];
+            sufz2[k] = sufz2[k + 1] + zeta[k] * zeta[k];
+        }
+        pre1.assign(L + 1, 0.0);
+        prez.assign(L + 1, 0.0);
+        for (size_t k = 0; k < L; ++k) {
+            pre1[k + 1] = pre1[k] + C[k];
+            prez[k + 1] = prez[k] + zeta[k];
+        }
         rest_sums();
+    }
+    // sort the candidates (positive doubles: their bit patterns order like their values)
+    // decreasingly, their zeta along: LSD radix on ~bits, 11-bit digits, passes that keep every key
+    // in one bucket skipped
+    static void radix_desc(std::vector<double>& C, std::vector<double>& Z)
+    {
+        const size_t N = C.size();
+        if (N < 2) return;
+        std::vector<uint64_t> k(N), k2(N);
+        std::vector<double> z2(N);
+        for (size_t i = 0; i < N; ++i) {
+            uint64_t b;
+            std::memcpy(&b, &C[i], 8);
+            k[i] = ~b;
+        }
+        constexpr int BITS = 11;
+        constexpr uint64_t NB = 1ull << BITS;
+        std::vector<uint32_t> cnt(NB);
+        for (int sh = 0; sh < 64; sh += BITS) {
+            std::fill(cnt.begin(), cnt.end(), 0u);
+            for (size_t i = 0; i < N; ++i) ++cnt[(k[i] >> sh) & (NB - 1)];
+            if (cnt[(k[0] >> sh) & (NB - 1)] == N) continue;
+            uint32_t acc = 0;
+            for (uint64_t b = 0; b < NB; ++b) {
+                const uint32_t c = cnt[b];
+                cnt[b] = acc;
+                acc += c;
+            }
+            for (size_t i = 0; i < N; ++i) {
+                const uint32_t p = cnt[(k[i] >> sh) & (NB - 1)]++;
+                k2[p] = k[i];
+                z2[p] = Z[i];
+            }
+            k.swap(k2);
+            Z.swap(z2);
+        }
+        for (size_t i = 0; i < N; ++i) {
+            const uint64_t b = ~k[i];
+            std::memcpy(&C[i], &b, 8);
+        }
     }
     void rest_sums()
     {
