@@ -1529,7 +1529,9 @@ struct LazyEstimator {
         constexpr int BITS = 11;
         constexpr uint64_t NB = 1ull << BITS;
         std::vector<uint32_t> cnt(NB);
-        for (int sh = 0; sh < 64; sh += BITS) {
+        // digits of the top 33 bits only (sign, exponent, 21 mantissa bits: keys equal there differ
+        // by < 2^-21 relative and are rare); the insertion pass below orders them by the full key
+        for (int sh = 31; sh < 64; sh += BITS) {
             std::fill(cnt.begin(), cnt.end(), 0u);
             for (size_t i = 0; i < N; ++i) ++cnt[(k[i] >> sh) & (NB - 1)];
             if (cnt[(k[0] >> sh) & (NB - 1)] == N) continue;
@@ -1546,6 +1548,19 @@ struct LazyEstimator {
             }
             k.swap(k2);
             Z.swap(z2);
+        }
+        for (size_t i = 1; i < N; ++i) {  // full-key order inside runs of equal top bits
+            const uint64_t ki = k[i];
+            if (!(k[i - 1] > ki)) continue;
+            const double zi = Z[i];
+            size_t j = i;
+            while (j > 0 && k[j - 1] > ki) {
+                k[j] = k[j - 1];
+                Z[j] = Z[j - 1];
+                --j;
+            }
+            k[j] = ki;
+            Z[j] = zi;
         }
         for (size_t i = 0; i < N; ++i) {
             const uint64_t b = ~k[i];
@@ -1698,6 +1713,7 @@ static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double
                 }
                 const auto tp1 = std::chrono::steady_clock::now();
                 E.reset();
+                const auto tp1b = std::chrono::steady_clock::now();
                 // ---- host search (exponential bracket, bisection in log kappa, R12) ----
                 const double k0 = out.kappa0;
                 double lo = 0, hi = 0, fv = 0, bad_kappa = 0;
@@ -1760,10 +1776,11 @@ static int scale_impl(const double* w, uint64_t n, double avg_deg, int d, double
                 static const bool dbg = getenv("GIRG_SCALE_DEBUG") != nullptr;
                 if (dbg) {
                     const auto tp2 = std::chrono::steady_clock::now();
-                    fprintf(stderr, "[girg scale] attempt %d ncand %u sorted %zu tau %g ok %d iters %d kappa0 %g device+copy %.3f ms search %.3f ms\n",
+                    fprintf(stderr, "[girg scale] attempt %d ncand %u sorted %zu tau %g ok %d iters %d kappa0 %g device+copy %.3f ms sort %.3f search %.3f ms\n",
                             attempt, out.ncand, E.L, E.tau, (int)ok, it, k0,
                             std::chrono::duration<double, std::milli>(tp1 - tp0).count(),
-                            std::chrono::duration<double, std::milli>(tp2 - tp1).count());
+                            std::chrono::duration<double, std::milli>(tp1b - tp1).count(),
+                            std::chrono::duration<double, std::milli>(tp2 - tp1b).count());
                 }
                 if (ok) {
                     *kappa_out = 0.5 * (lo + hi);
