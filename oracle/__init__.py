@@ -20,7 +20,7 @@ _SRC = os.path.join(_HERE, "girg_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 OK, EINVAL, ECAPACITY, ERANGE, ENOMEM = 0, -1, -2, -3, -4
-SCHEME_EVENT, SCHEME_MERGED = 0, 1  # type-II: per cell pair (Alg. 1 as written) / merged (R22)
+SCHEME_EVENT, SCHEME_MERGED, SCHEME_REFINED = 0, 1, 2  # type-II: per cell pair (Alg. 1 as written) / merged (R22) / refined bound (R27)
 
 
 def build(force: bool = False) -> str:
@@ -40,7 +40,7 @@ class Stats(C.Structure):
     _fields_ = [(name, C.c_uint64) for name in (
         "visits", "ev1", "ev1_nonempty", "cand1", "acc1",
         "ev2", "ev2_nonempty", "chunks", "draws", "landings", "acc2",
-        "nt1", "nt2acc", "nt2jump", "cand2", "ns_pre", "ns_edges", "rnd1", "jchk")]
+        "nt1", "nt2acc", "nt2jump", "cand2", "ns_pre", "ns_edges", "rnd1", "jchk", "bound_viol")]
 
     def as_dict(self):
         return {k: int(getattr(self, k)) for k, _ in self._fields_}

@@ -431,6 +431,7 @@ typedef struct {
     /* type-II tables per (i, j, level, class) */
     double *pbar, *Lbar;
     int *clog2;
+    double *pbarR, *LbarR; /* R27: per (i, j, level, class h = 2, 3, 4) */
     /* per-level bucket-pair lists: eq[l] = pairs with CL == l, ge[l] = CL >= l */
     int neq[33], nge[33];
     int eq[33][64 * 65 / 2][2];
@@ -452,6 +453,7 @@ typedef struct {
 } or_ctx;
 
 #define TAB(c, i, j, l, k) ((((size_t)(i) * 64 + (j)) * 32 + (l)) * 2 + (k))
+#define TAB3(c, i, j, l, k) ((((size_t)(i) * 64 + (j)) * 32 + (l)) * 3 + (k))
 
 static void emit(or_ctx *c, uint32_t u, uint32_t v)
 {
@@ -548,15 +550,20 @@ static void type2(or_ctx *c, int l, uint32_t A, uint32_t B, int i, int j)
     if (N == 0) return;
     c->st->ev2_nonempty++;
     c->st->cand2 += N;
-    if (c->cover) {
-        const uint32_t *Va = c->order + c->lstart[i], *Vb = c->order + c->lstart[j];
-        for (uint64_t s = a0; s < a1; s++)
-            for (uint64_t t = b0; t < b1; t++) c->cover[(uint64_t)Va[s] * c->n + Vb[t]]++;
-        return;
-    }
     int cls = or_delta_max(A, B, c->d, l) - 2; /* mind = (delta_max - 1) 2^-l, R9 */
     size_t ti = TAB(c, i, j, l, cls);
     double pbar = c->pbar[ti], Lbar = c->Lbar[ti];
+    if (c->cover) { /* every candidate once; and the bound must hold for each */
+        const uint32_t *Va = c->order + c->lstart[i], *Vb = c->order + c->lstart[j];
+        double xu[5], xv[5];
+        for (uint64_t s = a0; s < a1; s++)
+            for (uint64_t t = b0; t < b1; t++) {
+                c->cover[(uint64_t)Va[s] * c->n + Vb[t]]++;
+                double D = or_dpow(or_torus_dist(xcoord(c, Va[s], xu), xcoord(c, Vb[t], xv), c->d), c->d);
+                if (or_prob(c->w[Va[s]], c->w[Vb[t]], c->s, D, c->T) > pbar) c->st->bound_viol++;
+            }
+        return;
+    }
     if (pbar == 0.0) return;
     /* R10: chunk length C = 2^clog2 (2..4 expected landings per chunk), doubled until the
      * event has at most 2^15 chunks (the chunk index has 15 counter bits) */
@@ -675,10 +682,13 @@ static void distant_cells(const or_ctx *c, int l, uint32_t A, uint32_t *out2, in
     }
 }
 
-static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, const uint32_t *Bs, int nBs)
+/* One merged geometric-jump sequence (R22 / R27): rows = sorted positions [a0, a1) of layer i,
+ * columns = the concatenation of V_j^B over the cells Bs[0..nBs) (level l, in the given order),
+ * every candidate landed on with probability pbar, chunks of 2^cl2 candidates keyed by
+ * Philox counter (c0, chunk, tag, draw). */
+static void type2_seq(or_ctx *c, int l, uint32_t c0, uint64_t a0, uint64_t a1, int j, uint32_t tag,
+                      double pbar, double Lbar, const uint32_t *Bs, int nBs)
 {
-    uint64_t a0, a1;
-    vrange(c, i, A, l, &a0, &a1);
     uint64_t nA = a1 - a0;
     /* prefix of |V_j^B| over the concatenation (scratch owned by merged_all) */
     uint64_t *pre = c->mpre, *b0 = c->mb0;
@@ -693,16 +703,20 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
     if (N == 0) return;
     c->st->ev2_nonempty++;
     c->st->cand2 += N;
+    int i = (int)((tag >> 5) & 63u);
     const uint32_t *Va = c->order + c->lstart[i], *Vb = c->order + c->lstart[j];
-    if (c->cover) {
+    double xu[5], xv[5];
+    if (c->cover) { /* every candidate once; and the bound must hold for each */
         for (uint64_t s = a0; s < a1; s++)
             for (int t = 0; t < nBs; t++)
-                for (uint64_t v = b0[t]; v < b0[t] + (pre[t + 1] - pre[t]); v++)
-                    c->cover[(uint64_t)Va[s] * c->n + Vb[v]]++;
+                for (uint64_t v = b0[t]; v < b0[t] + (pre[t + 1] - pre[t]); v++) {
+                    uint32_t uu = Va[s], vv = Vb[v];
+                    c->cover[(uint64_t)uu * c->n + vv]++;
+                    double D = or_dpow(or_torus_dist(xcoord(c, uu, xu), xcoord(c, vv, xv), c->d), c->d);
+                    if (or_prob(c->w[uu], c->w[vv], c->s, D, c->T) > pbar) c->st->bound_viol++;
+                }
         return;
     }
-    size_t ti = TAB(c, i, j, l, k - 2);
-    double pbar = c->pbar[ti], Lbar = c->Lbar[ti];
     if (pbar == 0.0) return;
     int cl2 = 0;
     cl2 = 1 - ilogb(pbar);
@@ -711,14 +725,12 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
     while (((N - 1) >> cl2) >= (1ull << 32)) cl2++;
     uint64_t C = 1ull << cl2;
     uint64_t nch = (N - 1) / C + 1;
-    uint32_t tag = (uint32_t)l | ((uint32_t)i << 5) | ((uint32_t)j << 11) | ((uint32_t)(k - 2) << 17) | (1u << 18);
-    double xu[5], xv[5];
     for (uint64_t ch = 0; ch < nch; ch++) {
         c->st->chunks++;
         uint64_t start = ch * C, end = start + C < N ? start + C : N;
         int64_t pos = (int64_t)start - 1;
         for (uint32_t r = 0;; r++) {
-            uint32_t ctr[4] = {A, (uint32_t)ch, tag, r}, o[4];
+            uint32_t ctr[4] = {c0, (uint32_t)ch, tag, r}, o[4];
             or_philox4x32_10(ctr, c->seed, o);
             c->st->draws++;
             double rj = or_u53(o[0], o[1]), ra = or_u53(o[2], o[3]);
@@ -745,6 +757,71 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
             if (or_tie_mode & 2) ra = p / pbar + or_tie_delta;
             if (fabs(ra * pbar - p) < 1e-12 * pbar) c->st->nt2acc++;
             if (ra * pbar < p) { c->st->acc2++; emit(c, u, v); }
+        }
+    }
+}
+
+/* R22: one sequence per (A cell, class delta_max = k) over V_i^A x (V_j^B, B in Bs) */
+static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, const uint32_t *Bs, int nBs)
+{
+    uint64_t a0, a1;
+    vrange(c, i, A, l, &a0, &a1);
+    size_t ti = TAB(c, i, j, l, k - 2);
+    uint32_t tag = (uint32_t)l | ((uint32_t)i << 5) | ((uint32_t)j << 11) | ((uint32_t)(k - 2) << 17) | (1u << 18);
+    type2_seq(c, l, A, a0, a1, j, tag, c->pbar[ti], c->Lbar[ti], Bs, nBs);
+}
+
+/* R27 (refined bound): the rows of A are split by A's children a on level
+ * l+1 (contiguous in the sorted index while l+1 <= I(i), Lemma 1), and the distant cells B of A
+ * are classed by their box distance from a instead of from A: h = max over dimensions of the
+ * torus gap between a (one level-(l+1) cell) and B (two level-(l+1) cells), in units of
+ * 2^-(l+1); a pair (u in a, v in B) is at distance >= h 2^-(l+1) (P:486-491 with a tighter
+ * mind).  Classes k = 0, 1, 2 for h = 2, 3, >= 4 (bound taken at h = 2, 3, 4).  On l = I(i)
+ * the rows are A itself (a = A, h = 2 (delta_max - 1)). */
+static uint32_t half_gap(uint32_t a2, uint32_t b, uint32_t S2) /* a2: level l+1, b: level l */
+{
+    uint32_t dd = (2u * b + S2 - a2) % S2; /* B = [dd, dd+2) relative to a = [0, 1) */
+    if (dd == 0 || dd == S2 - 1) return 0;
+    uint32_t r = dd - 1, lft = S2 - dd - 2;
+    return r < lft ? r : lft;
+}
+
+static void type2_refined(or_ctx *c, int l, uint32_t A, int i, int j, const uint32_t *Bs, int nBs,
+                          uint32_t *cls[3])
+{
+    int d = c->d;
+    int sub = l + 1 <= c->lv.I[i];
+    uint32_t nsub = sub ? 1u << d : 1u;
+    uint32_t S2 = 2u << l, bc[5], acd[5];
+    for (uint32_t e = 0; e < nsub; e++) {
+        uint32_t a = sub ? (A << d) | e : A;
+        uint64_t a0, a1;
+        vrange(c, i, a, sub ? l + 1 : l, &a0, &a1);
+        if (a1 == a0) continue;
+        if (sub) or_morton_decode(a, d, l + 1, acd);
+        else {
+            or_morton_decode(A, d, l, acd);
+            for (int k = 0; k < d; k++) acd[k] *= 2u; /* a = A: its lower half, gap taken from A's box below */
+        }
+        int nk[3] = {0, 0, 0};
+        for (int t = 0; t < nBs; t++) {
+            or_morton_decode(Bs[t], d, l, bc);
+            uint32_t h = 0;
+            for (int k = 0; k < d; k++) {
+                uint32_t g = half_gap(acd[k], bc[k], S2);
+                if (!sub) { /* A = two level-(l+1) cells: the nearer of its halves */
+                    uint32_t g2 = half_gap(acd[k] + 1u, bc[k], S2);
+                    if (g2 < g) g = g2;
+                }
+                if (g > h) h = g;
+            }
+            int k = h <= 2 ? 0 : (h == 3 ? 1 : 2);
+            cls[k][nk[k]++] = Bs[t];
+        }
+        for (int k = 0; k < 3; k++) {
+            size_t ti = TAB3(c, i, j, l, k);
+            uint32_t tag = (uint32_t)l | ((uint32_t)i << 5) | ((uint32_t)j << 11) | ((uint32_t)k << 17) | (1u << 19);
+            type2_seq(c, l, a, a0, a1, j, tag, c->pbarR[ti], c->LbarR[ti], cls[k], nk[k]);
         }
     }
 }
@@ -824,6 +901,9 @@ static void merged_all(or_ctx *c)
     for (int k = 0; k < d; k++) noff *= 6;
     uint32_t *l2 = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)noff);
     uint32_t *l3 = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)noff);
+    uint32_t *all = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)noff);
+    uint32_t *cls[3];
+    for (int k = 0; k < 3; k++) cls[k] = (uint32_t *)malloc(sizeof(uint32_t) * (size_t)noff);
     c->mpre = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(noff + 1));
     c->mb0 = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(noff + 1));
     for (int l = 2; l <= c->lv.maxCL; l++)
@@ -850,6 +930,13 @@ static void merged_all(or_ctx *c)
                         while (s3 < n3 && l3[s3] <= A) s3++;
                     }
                     c->st->ev2 += (uint64_t)(n2 - s2 + n3 - s3);
+                    if (c->scheme == OR_SCHEME_REFINED) { /* both classes in one Morton-ordered list */
+                        int na = 0, p2 = s2, p3 = s3;
+                        while (p2 < n2 || p3 < n3)
+                            all[na++] = (p3 >= n3 || (p2 < n2 && l2[p2] < l3[p3])) ? l2[p2++] : l3[p3++];
+                        type2_refined(c, l, A, i, j, all, na, cls);
+                        continue;
+                    }
                     type2_merged(c, l, A, i, j, 2, l2 + s2, n2 - s2);
                     type2_merged(c, l, A, i, j, 3, l3 + s3, n3 - s3);
                 }
@@ -857,6 +944,8 @@ static void merged_all(or_ctx *c)
         }
     free(l2);
     free(l3);
+    free(all);
+    for (int k = 0; k < 3; k++) free(cls[k]);
     free(c->mpre);
     free(c->mb0);
 }
@@ -904,7 +993,7 @@ static int or_run_s(const double *w, const double *x, uint64_t n, int d, double 
     if (!(kappa > 0.0) || !isfinite(kappa)) return OR_EINVAL;
     if (shard_level < 0 || shard_level * d > 32 || blk_lo >= blk_hi) return OR_EINVAL;
     if (nranks > 0 && rank >= nranks) return OR_EINVAL;
-    if (scheme != OR_SCHEME_EVENT && scheme != OR_SCHEME_MERGED) return OR_EINVAL;
+    if (scheme != OR_SCHEME_EVENT && scheme != OR_SCHEME_MERGED && scheme != OR_SCHEME_REFINED) return OR_EINVAL;
     for (uint64_t i = 0; i < (uint64_t)d * n; i++)
         if (!(x[i] >= 0.0 && x[i] < 1.0)) return OR_EINVAL;
 
@@ -1006,6 +1095,26 @@ static int or_run_s(const double *w, const double *x, uint64_t n, int d, double 
                         c->clog2[t] = cl2;
                     }
             }
+        /* R27: classes h = 2, 3, 4: mind = h 2^-(l+1), mind^d = h^d 2^(-d(l+1)) (exact) */
+        size_t sz3 = (size_t)64 * 64 * 32 * 3;
+        c->pbarR = (double *)calloc(sz3, sizeof(double));
+        c->LbarR = (double *)calloc(sz3, sizeof(double));
+        if (!c->pbarR || !c->LbarR) { rc = OR_ENOMEM; goto done; }
+        for (int i = 0; i < L; i++)
+            for (int j = 0; j < L; j++) {
+                double qbar = ldexp(1.0, 2 * c->lv.e_min + i + j + 2) * c->s;
+                for (int l = 2; l <= c->lv.CL[i][j]; l++)
+                    for (int k = 0; k < 3; k++) {
+                        double hd = 1.0;
+                        for (int q = 0; q < d; q++) hd *= (double)(k + 2);
+                        double mind_d = ldexp(hd, -d * (l + 1));
+                        double ratio = qbar / mind_d;
+                        double pb = ratio >= 1.0 ? 1.0 : pow(ratio, c->invT);
+                        size_t t = TAB3(c, i, j, l, k);
+                        c->pbarR[t] = pb;
+                        c->LbarR[t] = log1p(-pb);
+                    }
+            }
     }
 
     if (ix) { /* test hook: export the index instead of sampling */
@@ -1027,7 +1136,7 @@ static int or_run_s(const double *w, const double *x, uint64_t n, int d, double 
     }
     uint64_t t1 = now_ns();
     recur(c, 0, 0u, 0u);
-    if (c->T > 0.0 && c->scheme == OR_SCHEME_MERGED) merged_all(c);
+    if (c->T > 0.0 && c->scheme != OR_SCHEME_EVENT) merged_all(c);
     st->ns_pre = t1 - t0;
     st->ns_edges = now_ns() - t1;
     rc = c->err;
@@ -1038,6 +1147,7 @@ done:
     free(c->order); free(c->codeI); free(cell); free(lay);
     for (int i = 0; i < 64; i++) free(c->P[i]);
     free(c->pbar); free(c->Lbar); free(c->clog2);
+    free(c->pbarR); free(c->LbarR);
     free(c);
     return rc;
 }

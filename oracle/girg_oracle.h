@@ -78,6 +78,7 @@ typedef struct {
     uint64_t ns_pre, ns_edges;     /* wall time: levels + index ("Pre"), recursion ("Edges") */
     uint64_t rnd1;                 /* type-I decisions that drew a uniform (p_uv < 1) */
     uint64_t jchk;                 /* jump near-tie checks (draws with z < remaining + 1) */
+    uint64_t bound_viol;           /* coverage mode: merged / refined candidates with p_uv > pbar */
 } or_stats_t;
 
 /* TEST HOOK (O12 pin): move type-I uniforms (bit 1), type-II acceptance uniforms (bit 2) or
@@ -89,6 +90,9 @@ void or_set_tie_hook(int mode, double delta);
  * the same bound concatenated (R22, exact in distribution; the product default). */
 #define OR_SCHEME_EVENT 0
 #define OR_SCHEME_MERGED 1
+/* REFINED = MERGED with the rows of A split by A's children on level l+1 and the distant cells
+ * classed by their box distance from the child (R27) */
+#define OR_SCHEME_REFINED 2
 
 /* Edge sampler: Algorithm 1 over the Lemma-1 index, double counting
  * per App. B.1 (R16), type-II by geometric jumps (R10 / R22).

@@ -40,7 +40,7 @@ def test_threshold_C1_full_bruteforce(oracle):
     assert st["ev2"] == 0  # no type-II events at T = 0
 
 
-SCHEMES = pytest.mark.parametrize("scheme", [0, 1], ids=["event", "merged"])
+SCHEMES = pytest.mark.parametrize("scheme", [0, 1, 2], ids=["event", "merged", "refined"])
 
 
 @SCHEMES
@@ -59,6 +59,8 @@ def test_coverage_each_pair_exactly_once(oracle, d, T, scheme):
     assert (sym[off] == 1).all()
     assert st["ev2_nonempty"] > 0 and st["ev1_nonempty"] > 0
     assert st["cand1"] + st["cand2"] == n * (n - 1) // 2
+    # the type-II bound of every candidate's sequence holds: p_uv <= pbar (R9, R27)
+    assert st["bound_viol"] == 0
 
 
 @SCHEMES
@@ -143,6 +145,25 @@ def test_merged_scheme_reduces_draws(oracle):
     assert sm["draws"] < 0.7 * se["draws"]
     z = abs(sm["landings"] - se["landings"]) / math.sqrt(se["landings"] + sm["landings"])
     assert z < 5, (se["landings"], sm["landings"])
+
+
+@pytest.mark.parametrize("d,T,beta,deg", [(3, 0.9, 2.9, 20.0), (2, 0.8, 2.2, 20.0)])
+def test_refined_scheme_cuts_landings(oracle, d, T, beta, deg):
+    """R27: the same candidate pairs and type-I work as R22, sequences per
+    (child of A, distance class) instead of per (A, delta_max), and markedly fewer landings for the
+    same edges in expectation (the bound of a far child is (3/2)^(d/T) or (5/4)^(d/T) smaller)."""
+    n = 20000
+    w, x = synth_inputs(n, d, beta, 5)
+    kappa = oracle.scale_weights(w, deg, d, T, beta)
+    em, sm = oracle.edges(w, x, d, T, kappa, 3, with_stats=True, scheme=1)
+    er, sr = oracle.edges(w, x, d, T, kappa, 3, with_stats=True, scheme=2)
+    assert sm["cand1"] == sr["cand1"] and sm["acc1"] == sr["acc1"]
+    assert sm["cand2"] == sr["cand2"]
+    assert sr["ev2_nonempty"] > 2 * sm["ev2_nonempty"]  # the children's sequences exist
+    assert sr["landings"] < (0.75 if d == 3 else 0.8) * sm["landings"], (sm["landings"], sr["landings"])
+    z = abs(sr["acc2"] - sm["acc2"]) / math.sqrt(sr["acc2"] + sm["acc2"])
+    assert z < 5, (sm["acc2"], sr["acc2"])
+    assert sr["nt1"] + sr["nt2acc"] + sr["nt2jump"] == 0
 
 
 @SCHEMES
