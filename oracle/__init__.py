@@ -106,6 +106,7 @@ def lib():
         L.or_index.argtypes = [dp, dp, u64, i32, d, u32p, u64p, u32p, u64p, u64]; L.or_index.restype = i32
         L.or_count_pairs.argtypes = [i32, i32, u64p, u64p, u64p, u64p]; L.or_count_pairs.restype = i32
         L.or_set_tie_hook.argtypes = [i32, d]
+        L.or_set_ref_x.argtypes = [i32]
         L.or_det_log.argtypes = [d]; L.or_det_log.restype = d
         L.or_det_exp.argtypes = [d]; L.or_det_exp.restype = d
         L.or_det_pow.argtypes = [d, d]; L.or_det_pow.restype = d
@@ -332,6 +333,12 @@ def det_pow(x, y):
 def set_tie_hook(mode: int, delta: float = 0.0):
     """TEST HOOK (O12 pin): perturb decision variables to threshold + delta (0 = off)."""
     lib().or_set_tie_hook(int(mode), float(delta))
+
+
+def set_ref_x(x: int):
+    """TEST HOOK (R27 pins at small n): REFINED threshold, 0 = default (8 points per cell),
+    k > 0 = k points, -1 = every level l < CL(i,j)."""
+    lib().or_set_ref_x(int(x))
 
 
 def sort_edges(e: np.ndarray) -> np.ndarray:

@@ -772,12 +772,23 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
 }
 
 /* R27 (refined bound): the rows of A are split by A's children a on level
- * l+1 (contiguous in the sorted index while l+1 <= I(i), Lemma 1), and the distant cells B of A
+ * l+1 (contiguous in the sorted index because l+1 <= I(i), Lemma 1), and the distant cells B of A
  * are classed by their box distance from a instead of from A: h = max over dimensions of the
  * torus gap between a (one level-(l+1) cell) and B (two level-(l+1) cells), in units of
  * 2^-(l+1); a pair (u in a, v in B) is at distance >= h 2^-(l+1) (P:486-491 with a tighter
- * mind).  Classes k = 0, 1, 2 for h = 2, 3, >= 4 (bound taken at h = 2, 3, 4).  On l = I(i)
- * the rows are A itself (a = A, h = 2 (delta_max - 1)). */
+ * mind).  Classes k = 0, 1, 2 for h = 2, 3, >= 4 (bound taken at h = 2, 3, 4).  Applied where
+ * ref_level() says (R27). */
+#define OR_REF_X 8 /* R27: refine a level when layer i has >= 8 points per level-l cell on average */
+static int or_ref_x = 0;  /* TEST HOOK: 0 = OR_REF_X, k > 0 = k points, -1 = every level l < CL */
+void or_set_ref_x(int x) { or_ref_x = x; }
+
+static int ref_level(const or_ctx *c, int l, int i, int j)
+{
+    long x = or_ref_x == 0 ? OR_REF_X : or_ref_x;
+    return c->scheme == OR_SCHEME_REFINED && (c->d == 2 || c->d == 3) && l < c->lv.CL[i][j] &&
+           (x < 0 || (uint64_t)c->lv.cnt[i] >= ((uint64_t)x << (c->d * l)));
+}
+
 static uint32_t half_gap(uint32_t a2, uint32_t b, uint32_t S2) /* a2: level l+1, b: level l */
 {
     uint32_t dd = (2u * b + S2 - a2) % S2; /* B = [dd, dd+2) relative to a = [0, 1) */
@@ -790,29 +801,19 @@ static void type2_refined(or_ctx *c, int l, uint32_t A, int i, int j, const uint
                           uint32_t *cls[3])
 {
     int d = c->d;
-    int sub = l + 1 <= c->lv.I[i];
-    uint32_t nsub = sub ? 1u << d : 1u;
     uint32_t S2 = 2u << l, bc[5], acd[5];
-    for (uint32_t e = 0; e < nsub; e++) {
-        uint32_t a = sub ? (A << d) | e : A;
+    for (uint32_t e = 0; e < (1u << d); e++) {
+        uint32_t a = (A << d) | e; /* child of A on level l+1 <= I(i) */
         uint64_t a0, a1;
-        vrange(c, i, a, sub ? l + 1 : l, &a0, &a1);
+        vrange(c, i, a, l + 1, &a0, &a1);
         if (a1 == a0) continue;
-        if (sub) or_morton_decode(a, d, l + 1, acd);
-        else {
-            or_morton_decode(A, d, l, acd);
-            for (int k = 0; k < d; k++) acd[k] *= 2u; /* a = A: its lower half, gap taken from A's box below */
-        }
+        or_morton_decode(a, d, l + 1, acd);
         int nk[3] = {0, 0, 0};
         for (int t = 0; t < nBs; t++) {
             or_morton_decode(Bs[t], d, l, bc);
             uint32_t h = 0;
             for (int k = 0; k < d; k++) {
                 uint32_t g = half_gap(acd[k], bc[k], S2);
-                if (!sub) { /* A = two level-(l+1) cells: the nearer of its halves */
-                    uint32_t g2 = half_gap(acd[k] + 1u, bc[k], S2);
-                    if (g2 < g) g = g2;
-                }
                 if (g > h) h = g;
             }
             int k = h <= 2 ? 0 : (h == 3 ? 1 : 2);
@@ -930,7 +931,7 @@ static void merged_all(or_ctx *c)
                         while (s3 < n3 && l3[s3] <= A) s3++;
                     }
                     c->st->ev2 += (uint64_t)(n2 - s2 + n3 - s3);
-                    if (c->scheme == OR_SCHEME_REFINED) { /* both classes in one Morton-ordered list */
+                    if (ref_level(c, l, i, j)) { /* R27: both classes in one Morton-ordered list */
                         int na = 0, p2 = s2, p3 = s3;
                         while (p2 < n2 || p3 < n3)
                             all[na++] = (p3 >= n3 || (p2 < n2 && l2[p2] < l3[p3])) ? l2[p2++] : l3[p3++];

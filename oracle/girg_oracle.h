@@ -90,9 +90,14 @@ void or_set_tie_hook(int mode, double delta);
  * the same bound concatenated (R22, exact in distribution; the product default). */
 #define OR_SCHEME_EVENT 0
 #define OR_SCHEME_MERGED 1
-/* REFINED = MERGED with the rows of A split by A's children on level l+1 and the distant cells
- * classed by their box distance from the child (R27) */
+/* REFINED = MERGED, except on the levels l < CL(i,j) where layer i has >= 8 points per level-l
+ * cell on average (d = 2, 3): there the rows of A are split by A's children on level l+1 and the
+ * distant cells classed by their box distance from the child (R27) */
 #define OR_SCHEME_REFINED 2
+/* TEST HOOK (pins of R27 at small n): the REFINED scheme's points-per-cell threshold; 0 = the
+ * default (8), k > 0 = k, -1 = every level l < CL(i,j).  The library's girg_options.ref_x has the
+ * same meaning. */
+void or_set_ref_x(int x);
 
 /* Edge sampler: Algorithm 1 over the Lemma-1 index, double counting
  * per App. B.1 (R16), type-II by geometric jumps (R10 / R22).

@@ -40,7 +40,21 @@ def test_threshold_C1_full_bruteforce(oracle):
     assert st["ev2"] == 0  # no type-II events at T = 0
 
 
-SCHEMES = pytest.mark.parametrize("scheme", [0, 1, 2], ids=["event", "merged", "refined"])
+# "refined_all": R27 on every level l < CL(i,j) (the ref_x test hook), so that the small pin
+# graphs exercise the refined sequences, which the default threshold (8 points per cell) only
+# reaches at larger n
+SCHEMES = pytest.mark.parametrize("scheme", [0, 1, 2, "refined_all"], ids=["event", "merged", "refined", "refined_all"],
+                                  indirect=True)
+
+
+@pytest.fixture
+def scheme(request, oracle):
+    if request.param == "refined_all":
+        oracle.set_ref_x(-1)
+        yield 2
+        oracle.set_ref_x(0)
+    else:
+        yield request.param
 
 
 @SCHEMES
@@ -68,9 +82,28 @@ def test_coverage_each_pair_exactly_once(oracle, d, T, scheme):
 def test_per_pair_frequency(oracle, d, T, runs, scheme):
     """with fixed w and x, each pair's empirical edge frequency over independent edge
     seeds is within 5 sigma of p_uv (Eq. 1), and the chi-square over pairs is plausible."""
-    n = 40
+    per_pair_check(oracle, 40, d, T, runs, 3.0, scheme)
+
+
+def test_refined_per_pair_frequency_d3(oracle):
+    """The same pin for R27 in d = 3 on a graph where its rows are split (n = 64, low degree:
+    CL(0,0) = 3, so level 2 is refined under the every-level hook; the n = 40 graph above has no
+    level below CL)."""
+    oracle.set_ref_x(-1)
+    try:
+        w, x = synth_inputs(64, 3, 2.5, 8)
+        kappa = oracle.scale_weights(w, 1.0, 3, 0.9, 2.5)
+        sm = oracle.edges(w, x, 3, 0.9, kappa, 1, with_stats=True, scheme=1)[1]
+        sr = oracle.edges(w, x, 3, 0.9, kappa, 1, with_stats=True, scheme=2)[1]
+        assert sr["ev2_nonempty"] > sm["ev2_nonempty"]  # refined sequences exist
+        per_pair_check(oracle, 64, 3, 0.9, 5000, 1.0, 2)
+    finally:
+        oracle.set_ref_x(0)
+
+
+def per_pair_check(oracle, n, d, T, runs, deg, scheme):
     w, x = synth_inputs(n, d, 2.5, 5 + d)
-    kappa = oracle.scale_weights(w, 3.0, d, T, 2.5)
+    kappa = oracle.scale_weights(w, deg, d, T, 2.5)
     W = oracle.exact_sum(w)
     s = kappa / W
     P = np.zeros((n, n))
@@ -149,18 +182,19 @@ def test_merged_scheme_reduces_draws(oracle):
 
 @pytest.mark.parametrize("d,T,beta,deg", [(3, 0.9, 2.9, 20.0), (2, 0.8, 2.2, 20.0)])
 def test_refined_scheme_cuts_landings(oracle, d, T, beta, deg):
-    """R27: the same candidate pairs and type-I work as R22, sequences per
-    (child of A, distance class) instead of per (A, delta_max), and markedly fewer landings for the
-    same edges in expectation (the bound of a far child is (3/2)^(d/T) or (5/4)^(d/T) smaller)."""
-    n = 20000
+    """R27: the same candidate pairs and type-I work as R22; on the refined
+    levels (l < CL(i,j), >= 8 points of layer i per cell) sequences per (child of A, distance
+    class) instead of per (A, delta_max), and markedly fewer landings for the same edges in
+    expectation (the bound of a far child is (2/3)^(d/T) of A's)."""
+    n = 60000
     w, x = synth_inputs(n, d, beta, 5)
     kappa = oracle.scale_weights(w, deg, d, T, beta)
     em, sm = oracle.edges(w, x, d, T, kappa, 3, with_stats=True, scheme=1)
     er, sr = oracle.edges(w, x, d, T, kappa, 3, with_stats=True, scheme=2)
     assert sm["cand1"] == sr["cand1"] and sm["acc1"] == sr["acc1"]
     assert sm["cand2"] == sr["cand2"]
-    assert sr["ev2_nonempty"] > 2 * sm["ev2_nonempty"]  # the children's sequences exist
-    assert sr["landings"] < (0.75 if d == 3 else 0.8) * sm["landings"], (sm["landings"], sr["landings"])
+    assert sr["ev2_nonempty"] > 1.4 * sm["ev2_nonempty"]  # the children's sequences exist
+    assert sr["landings"] < (0.87 if d == 3 else 0.92) * sm["landings"], (sm["landings"], sr["landings"])
     z = abs(sr["acc2"] - sm["acc2"]) / math.sqrt(sr["acc2"] + sm["acc2"])
     assert z < 5, (sm["acc2"], sr["acc2"])
     assert sr["nt1"] + sr["nt2acc"] + sr["nt2jump"] == 0
