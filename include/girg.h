@@ -124,16 +124,23 @@ int girg_edges_shard(const double *w_dev, const double *x_dev, uint64_t n, int d
                      uint64_t blk_hi, uint32_t *edges_dev, uint64_t cap, uint64_t *m_out,
                      girg_stats *stats_out, void *stream);
 
-/* type-II sampling schemes (R10 / R22).  Both give exactly the GIRG distribution;
+/* type-II sampling schemes (R10 / R22 / R27).  Each gives exactly the GIRG distribution;
  * for a fixed seed they give different (each deterministic) edge sets. */
 #define GIRG_SCHEME_EVENT 0  /* one geometric-jump sequence per distant cell pair: Alg. 1 lines 5-6
                                 as written, chunks of 2..4 expected landings */
 #define GIRG_SCHEME_MERGED 1 /* default: the distant cells of an A cell with the same bound class
                                 concatenated into one sequence (memorylessness of the jumps,
                                 P:494-501), chunks of 2..4 expected landings */
+#define GIRG_SCHEME_REFINED 2 /* MERGED with the refined bound of DESIGN.md R27 (P:486-491 with a
+                                tighter minimum distance) where it pays: for d = 2, 3, T > 0, on the
+                                levels l < CL(i,j) with >= 8 points of layer i per cell, the rows of
+                                an A cell are split by A's children on level l+1 and its distant
+                                cells classed by their box distance from the child (2, 3, >= 4
+                                half-cells), one sequence per (child, class).  Elsewhere (and for
+                                other d or T = 0) identical to MERGED */
 
 typedef struct {
-    int scheme;           /* GIRG_SCHEME_MERGED (default) or GIRG_SCHEME_EVENT */
+    int scheme;           /* GIRG_SCHEME_MERGED (default), GIRG_SCHEME_EVENT or GIRG_SCHEME_REFINED */
     int shard_level;      /* as girg_edges_shard; 0, [0, 1) = the whole graph */
     uint64_t blk_lo, blk_hi;
     /* interleaved multi-GPU ownership (nranks > 0; blk_lo / blk_hi are then ignored): an event
@@ -256,6 +263,11 @@ const char *girg_last_cuda_error(void);
 
 /* Library ABI version (major*100 + minor). */
 int girg_version(void);
+
+/* TEST HOOK (not part of the product API): threshold of GIRG_SCHEME_REFINED's level rule, in
+ * points of layer i per level-l cell: 0 = the default (8), k > 0 = k points, -1 = every level
+ * l < CL(i,j), so that small parity cases exercise refined sequences.  Process-wide.  Returns 0. */
+int girg_debug_set_ref_x(int x);
 
 #ifdef __cplusplus
 }

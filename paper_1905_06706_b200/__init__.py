@@ -23,7 +23,7 @@ if os.environ.get("GIRG_LIBRARY"):  # e.g. the bounds-checked libgirg_debug.so
     _LIB_PATH = os.environ["GIRG_LIBRARY"]
 
 OK, EINVAL, ECAPACITY, ERANGE, ENOMEM, ECUDA = 0, -1, -2, -3, -4, -5
-SCHEME_EVENT, SCHEME_MERGED = 0, 1  # include/girg.h GIRG_SCHEME_*
+SCHEME_EVENT, SCHEME_MERGED, SCHEME_REFINED = 0, 1, 2  # include/girg.h GIRG_SCHEME_*
 
 if not os.path.exists(_LIB_PATH):
     raise ImportError(
@@ -74,12 +74,13 @@ _lib.girg_strerror.restype = C.c_char_p
 _lib.girg_last_cuda_error.restype = C.c_char_p
 for _f in ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
            "girg_edges_ex", "girg_edges_host", "girg_edges_batch", "girg_version", "girg_last_timings",
-           "girg_hrg_points", "girg_hrg_edges"):
+           "girg_hrg_points", "girg_hrg_edges", "girg_debug_set_ref_x"):
     getattr(_lib, _f).restype = C.c_int
+_lib.girg_debug_set_ref_x.argtypes = [_i]
 
 EXPORTS = ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
            "girg_edges_ex", "girg_edges_host", "girg_edges_batch", "girg_strerror", "girg_last_cuda_error", "girg_version",
-           "girg_last_timings", "girg_hrg_points", "girg_hrg_edges")
+           "girg_last_timings", "girg_hrg_points", "girg_hrg_edges", "girg_debug_set_ref_x")
 
 
 class GirgError(RuntimeError):
@@ -128,6 +129,11 @@ def library_path() -> str:
 
 def version() -> int:
     return _lib.girg_version()
+
+
+def debug_set_ref_x(x: int) -> None:
+    """TEST HOOK (include/girg.h girg_debug_set_ref_x): SCHEME_REFINED's level threshold."""
+    _check(_lib.girg_debug_set_ref_x(int(x)))
 
 
 def weights(n: int, beta: float, seed: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:

@@ -708,8 +708,20 @@ struct HostPlan {
 };
 
 // H6: layers, levels and bound tables; R5-R7, R9, R10.
+// R27 (refined type-II bound): level l of layer pair (i, j) is refined where it pays -- d = 2, 3,
+// T > 0, l < CL(i,j) (no type-I events on that level, and l + 1 <= I(i)) and at least REF_X points
+// of layer i per level-l cell on average (R27; the oracle's ref_level()).
+constexpr long REF_X = 8;
+static std::atomic<int> g_ref_x{0};  // TEST HOOK (girg_debug_set_ref_x): 0 = REF_X, k > 0 = k points, -1 = every l < CL
+static bool ref_level(int scheme, int d, double T, int l, int cl, uint64_t cnt_i)
+{
+    const long x = g_ref_x.load() == 0 ? REF_X : (long)g_ref_x.load();
+    return scheme == SCHEME_REFINED && (d == 2 || d == 3) && T > 0.0 && l < cl &&
+           (x < 0 || cnt_i >= ((uint64_t)x << (d * l)));
+}
+
 static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WPartial>& parts, uint64_t n, int d,
-                     double T, double kappa, HostPlan& hp, double s_override = 0.0)
+                     double T, double kappa, HostPlan& hp, double s_override = 0.0, int scheme = SCHEME_MERGED)
 {
     Plan& p = hp.p;
     std::memset(&p, 0, sizeof(p));
@@ -772,9 +784,17 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
                 p.tab_off[i * MAXL + j] = (uint32_t)hp.tab.size();
                 if (!p.cnt[i] || !p.cnt[j] || cl < 2) continue;
                 const double qbar = std::ldexp(1.0, 2 * emin + i + j + 2) * p.s;
+                // REFINED plans: 5 entries per level -- classes 2, 3, then the refined classes
+                // h = 2, 3, 4 half-cells: mind^d = h^d 2^(-d(l+1)) (exact; R27)
+                const int nk = scheme == SCHEME_REFINED ? 5 : 2;
                 for (int l = 2; l <= cl; ++l)
-                    for (int k = 0; k < 2; ++k) {
-                        const double mind_d = std::ldexp(1.0, -d * l + d * k);  // ((k+1) 2^-l)^d
+                    for (int k = 0; k < nk; ++k) {
+                        double mind_d = std::ldexp(1.0, -d * l + d * k);  // ((k+1) 2^-l)^d
+                        if (k >= 2) {
+                            double hd = 1.0;
+                            for (int q = 0; q < d; ++q) hd *= (double)k;  // h = k - 2 + 2
+                            mind_d = std::ldexp(hd, -d * (l + 1));
+                        }
                         const double ratio = qbar / mind_d;
                         TabEntry e;
                         e.pbar = ratio >= 1.0 ? 1.0 : std::pow(ratio, p.invT);
@@ -814,6 +834,10 @@ static int make_plan(const std::vector<uint32_t>& hist, const std::vector<WParti
                     const int lg = std::max(0, l - G);
                     const int t1 = l == cl, t2 = T > 0.0 && l >= 2;
                     if (!t1 && !t2) continue;
+                    if (t2 && ref_level(scheme, d, T, l, cl, p.cnt[i])) {  // R27: one job per A cell on level l (bit 14)
+                        E.emplace_back(l, (uint16_t)(j | (l << 6) | (t2 << 13) | (1 << 14)));
+                        continue;
+                    }
                     E.emplace_back(lg, (uint16_t)(j | (l << 6) | (t1 << 12) | (t2 << 13)));
                 }
             }
@@ -987,6 +1011,11 @@ static void launch_sample(const SampleArgs& a, int scheme, cudaStream_t st)
     } else if (scheme == SCHEME_EVENT) {
         if (a.stats) launch_sample_t<D, SCHEME_EVENT, true>(a, st);
         else launch_sample_t<D, SCHEME_EVENT, false>(a, st);
+    } else if (scheme == SCHEME_REFINED && (D == 2 || D == 3)) {
+        if constexpr (D == 2 || D == 3) {
+            if (a.stats) launch_sample_t<D, SCHEME_REFINED, true>(a, st);
+            else launch_sample_t<D, SCHEME_REFINED, false>(a, st);
+        }
     } else {
         if (a.stats) launch_sample_t<D, SCHEME_MERGED, true>(a, st);
         else launch_sample_t<D, SCHEME_MERGED, false>(a, st);
@@ -1042,7 +1071,7 @@ struct EdgeCall {
     static int validate(const double* w, const double* x, uint64_t n, int d, double T, double kappa, int sl,
                         uint64_t blo, uint64_t bhi, int scheme, uint32_t* edges, uint64_t cap, uint64_t* m_out)
     {
-        if (scheme != SCHEME_EVENT && scheme != SCHEME_MERGED) return GIRG_EINVAL;
+        if (scheme != SCHEME_EVENT && scheme != SCHEME_MERGED && scheme != SCHEME_REFINED) return GIRG_EINVAL;
         if (!w || !x || !m_out || (cap && !edges)) return GIRG_EINVAL;
         if (n == 0 || n >= (1ull << 32) || d < 1 || d > 5) return GIRG_EINVAL;
         if (!(T >= 0.0 && T < 1.0) || !(kappa > 0.0) || !std::isfinite(kappa)) return GIRG_EINVAL;
@@ -1079,7 +1108,9 @@ struct EdgeCall {
         std::memcpy(parts.data(), wst_host + HIST_BINS * sizeof(uint32_t) + 16, nb * sizeof(WPartial));
         if (herr & ERR_WEIGHT) { rc = GIRG_EINVAL; return; }
         if (herr & ERR_WRANGE) { rc = GIRG_ERANGE; return; }
-        rc = make_plan(hist, parts, n, d, T, kappa, hp, s_override);
+        // the refined bound exists for d = 2, 3 and T > 0 (R27); elsewhere REFINED is MERGED
+        if (scheme == SCHEME_REFINED && !((d == 2 || d == 3) && T > 0.0)) scheme = SCHEME_MERGED;
+        rc = make_plan(hist, parts, n, d, T, kappa, hp, s_override, scheme);
         if (rc) return;
         hp.p.sl = sl;
         hp.p.blo = blo;
@@ -2297,4 +2328,9 @@ extern "C" int girg_last_timings(girg_timings* out)
 
 extern "C" const char* girg_last_cuda_error(void) { return girg::g_last_cuda.c_str(); }
 
-extern "C" int girg_version(void) { return 200; }
+extern "C" int girg_version(void) { return 201; }
+extern "C" int girg_debug_set_ref_x(int x)
+{
+    girg::g_ref_x.store(x);
+    return GIRG_OK;
+}

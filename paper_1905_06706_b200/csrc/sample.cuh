@@ -44,7 +44,14 @@
     } while (0)
 #endif
 
-constexpr int SCHEME_EVENT = 0, SCHEME_MERGED = 1;
+constexpr int SCHEME_EVENT = 0, SCHEME_MERGED = 1, SCHEME_REFINED = 2;
+// index of a type-II kind (1, 2) in the JobInfo bound arrays: kind - KOFF.  The REFINED
+// instantiation (R27) stores them at [kind], because a refined job's three kinds 0..2 are all
+// jump-chain sequences (classes h = 2, 3, >= 4) with bounds at [0..2].
+template <int SCHEME>
+struct KOff {
+    static constexpr int v = SCHEME == SCHEME_REFINED ? 0 : 1;
+};
 // Unrolling of the job setup's shared-memory loops (runtime trip counts; nvcc unrolls them 4x by
 // default).  The sampling kernels are instruction-fetch bound as much as issue bound (ncu C5:
 // no_instructions is the top stall reason, the hot code is ~33 KB against a 32 KB L1.5 I$), so
@@ -218,18 +225,21 @@ struct SampleArgs {
 
 struct TaskDesc {
     int i, j, l, t1, t2;
+    int ref;           // R27 refined job (task bit 14): Cpar is the A cell on level l, its rows split by A's children
     uint32_t Cpar;     // the task cell Cg, on level lg = max(0, l - G)
     int lg, npar, cs;  // task level, region parents, child shift d (l - lg)
 };
 
 // per-job constants read by the lanes
 struct JobInfo {
-    double pbar[2], Lbar[2];  // type-II bounds of kinds 1, 2 (R9)
-    double il2[2];            // 1 / log2(1 - pbar) (fast jump path)
+    double pbar[3], Lbar[3];  // type-II bounds of kinds 1, 2 (R9) at [kind - KOff]; a refined job's classes at [0..2] (R27)
+    double il2[3];            // 1 / log2(1 - pbar) (fast jump path)
     int clog2[2];             // EVENT chunk length (R10)
-    int clog2m[2];            // MERGED chunk length (R22)
-    uint32_t tag;             // l | i<<5 | j<<11
+    int clog2m[3];            // MERGED / REFINED chunk length (R22)
+    uint32_t tag;             // l | i<<5 | j<<11 (REFINED instantiation: + the scheme bits, so that the
+                              // Philox tag word is tag + (kind << 17))
     int npar, cs, same_layer;
+    int ref;                  // refined job (REFINED instantiation only)
 };
 
 template <int D>
@@ -436,6 +446,7 @@ __device__ __forceinline__ TaskDesc make_task(int i, uint16_t task, uint32_t Cpa
     t.l = (task >> 6) & 63;
     t.t1 = (task >> 12) & 1;
     t.t2 = (task >> 13) & 1;
+    t.ref = (task >> 14) & 1;
     t.Cpar = Cpar;
     t.lg = max(0, t.l - Geo<D>::G);
     t.cs = D * (t.l - t.lg);
@@ -476,29 +487,37 @@ __device__ __noinline__ bool owns(const SampleArgs& a, uint32_t A, int l, int i,
 // ---- job setup, common part (warp-collective): region parents in Morton order, the Lemma-1
 // ranges of their sub-cells (layer j) and of the task cell's children (layer i), the nonempty
 // owned children of this batch, the job constants.  Returns the batch's child count.
-template <int D, class SL>
+template <int D, int SCHEME, class SL>
 __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const TaskDesc& t, int batch, JobSetup& out,
                                             const TabEntry*& te)
 {
     constexpr int CB = SL::CB;
+    // R27 refined job (REFINED instantiation, task bit 14): t.Cpar is the A cell on level l; its
+    // rows are A's children on level l + 1 (<= I(i)), the region is that of A's parent
+    constexpr bool RS = SCHEME == SCHEME_REFINED;
+    const bool ref = RS && t.ref;
+    const uint32_t Cg = ref ? t.Cpar >> D : t.Cpar;  // centre of the region, on level lg
     const Plan* pl = a.pl;
     const unsigned lane = lane_id();
     const int nsub = 1 << t.cs;
     // sharded runs: a task cell on or below the split level lies in one shard block, so a job of
     // another shard is dropped before any setup work
-    if (a.sharded && t.lg >= a.sl && !owns<D>(a, t.Cpar << t.cs, t.l, t.i, t.j)) {
+    if (a.sharded && (ref ? t.l : t.lg) >= a.sl && !owns<D>(a, ref ? t.Cpar : t.Cpar << t.cs, t.l, t.i, t.j)) {
         out.nchild = 0;
         return 0;
     }
     // the type-II bounds of the job (lanes 0, 1: classes 2, 3), loaded before the region so that
     // their latency overlaps the region loads
-    te = t.t2 ? a.tab + (pl->tab_off[t.i * MAXL + t.j] + 2u * (uint32_t)(t.l - 2)) : nullptr;
+    // (REFINED plans hold 5 entries per level: classes 2, 3 and the refined classes h = 2, 3, >= 4)
+    constexpr uint32_t TS = RS ? 5u : 2u;
+    const unsigned nte = ref ? 3u : 2u;
+    te = t.t2 ? a.tab + (pl->tab_off[t.i * MAXL + t.j] + TS * (uint32_t)(t.l - 2) + (ref ? 2u : 0u)) : nullptr;
     TabEntry tev = {0.0, 0.0, 0, 0, 0.0, 0.0};
-    if (te && lane < 2) tev = te[lane];
+    if (te && lane < nte) tev = te[lane];
     // ---- region parents in Morton order ----
     if (t.lg >= 2) {
         uint32_t pc[D];
-        morton_decode<D>(t.Cpar, pc);
+        morton_decode<D>(Cg, pc);
         const uint32_t mask = (1u << t.lg) - 1u;
         SETUP_LOOP
         for (int q = lane; q < t.npar; q += 32) {
@@ -537,7 +556,7 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
     __syncwarp();
     // ---- Lemma-1 ranges of the region sub-cells (layer j) and of Cg's children (layer i) ----
     {
-        const int shj = D * ((int)pl->I[t.j] - t.l), shi = D * ((int)pl->I[t.i] - t.l);
+        const int shj = D * ((int)pl->I[t.j] - t.l), shi = D * ((int)pl->I[t.i] - t.l - (ref ? 1 : 0));
         const uint32_t bj = pl->base[t.j], bi = pl->base[t.i];
         const int per = nsub + 1;
         constexpr int PER1 = Geo<D>::NCH + 1;  // per when l >= lg + G (the common case): a constant divisor
@@ -564,7 +583,7 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
             bool ok = false;
             if (e < nsub) {
                 ok = S.achild[e + 1] > S.achild[e];
-                const uint32_t A = (t.Cpar << t.cs) + (uint32_t)e;
+                const uint32_t A = ref ? t.Cpar : (t.Cpar << t.cs) + (uint32_t)e;
                 ok = ok && (!a.sharded || owns<D>(a, A, t.l, t.i, t.j));
             }
             const unsigned bm = __ballot_sync(FULL, ok);
@@ -578,18 +597,20 @@ __device__ __forceinline__ int setup_common(const SampleArgs& a, SL& S, const Ta
     if (nc <= 0) return 0;
     if (lane == 0) {
         JobInfo& J = S.job;
-        J.tag = (uint32_t)t.l | ((uint32_t)t.i << 5) | ((uint32_t)t.j << 11);
+        J.tag = ((uint32_t)t.l | ((uint32_t)t.i << 5) | ((uint32_t)t.j << 11)) + (RS ? (ref ? (1u << 19) : (1u << 17)) : 0u);
         J.npar = t.npar;
         J.cs = t.cs;
         J.same_layer = t.i == t.j;
+        J.ref = ref;
     }
-    if (lane < 2) {
+    if (lane < nte) {
         JobInfo& J = S.job;
-        J.pbar[lane] = tev.pbar;
-        J.Lbar[lane] = tev.Lbar;
-        J.il2[lane] = tev.il2;
-        J.clog2[lane] = tev.clog2;
-        J.clog2m[lane] = tev.clog2m;
+        const unsigned ix = ref ? lane : lane + 1u - (unsigned)KOff<SCHEME>::v;
+        J.pbar[ix] = tev.pbar;
+        J.Lbar[ix] = tev.Lbar;
+        J.il2[ix] = tev.il2;
+        if (lane < 2) J.clog2[lane] = tev.clog2;
+        J.clog2m[ix] = tev.clog2m;
     }
     __syncwarp();
     return nc;
@@ -604,7 +625,7 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
     const unsigned lane = lane_id();
     const int nsub = 1 << t.cs;
     const TabEntry* te = nullptr;
-    const int nc = setup_common<D>(a, S, t, batch, out, te);
+    const int nc = setup_common<D, SCHEME>(a, S, t, batch, out, te);
     if (nc <= 0) return out;
     // ---- phase 1: classify every (child, region parent) pair in parallel ----
     const int subl = t.cs / D;  // levels between a region parent and its sub-cells
@@ -637,7 +658,7 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
 #pragma unroll
                 for (int k = 0; k <= NCH; ++k) rs[k] = S.rstart[q][k];
                 uint32_t cnt[3] = {0u, 0u, 0u}, m[3] = {0u, 0u, 0u};
-                if constexpr (SCHEME == SCHEME_MERGED) {
+                if constexpr (SCHEME != SCHEME_EVENT) {
                     // Sub-cell sets as bit masks: {s : max_k gap_k(s) <= tau} is the AND over the
                     // dimensions of the sub-cells whose own gap in that dimension is <= tau.
                     constexpr uint32_t FULLN = (1u << NCH) - 1u;
@@ -798,9 +819,9 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
                 units[h] = (unsigned long long)Q.nA * acc;
             } else if (SCHEME == SCHEME_EVENT) {
                 units[h] = acc;
-            } else if (acc && S.job.pbar[k - 1] > 0.0) {
+            } else if (acc && S.job.pbar[k - KOff<SCHEME>::v] > 0.0) {
                 const unsigned long long N = (unsigned long long)Q.nA * acc;
-                Q.cl2 = chunk_log2(N, S.job.clog2m[k - 1], 32);
+                Q.cl2 = chunk_log2(N, S.job.clog2m[k - KOff<SCHEME>::v], 32);
                 units[h] = ((N - 1) >> Q.cl2) + 1;
             }
         }
@@ -828,6 +849,121 @@ __device__ __noinline__ JobSetup setup_job(const SampleArgs& a, Slot<D>& S, cons
     return out;
 }
 
+// R27 refined job (REFINED instantiation; R27: P:486-491 with a tighter minimum
+// distance).  The task cell is the A cell on level l < CL(i,j); its rows are split by A's
+// children a on level l + 1 (<= I(i)), and every distant cell B of A with a neighbouring parent
+// (the region sub-cells that are not neighbours of A) is classed by its box distance from a in
+// half-cells: h = max over the dimensions of the torus gap between a (one level-(l+1) cell) and
+// B (two of them), kinds 0, 1, 2 = h 2, 3, >= 4.  One merged sequence (R22) per (a, class), its
+// chunks keyed (a, chunk, l | i<<5 | j<<11 | class<<17 | 1<<19, draw).
+template <int D>
+__device__ __noinline__ JobSetup setup_job_ref(const SampleArgs& a, Slot<D>& S, const TaskDesc t, int batch)
+{
+    JobSetup out = {0ull, 0ull, 0, 0};
+    constexpr int NCH = Geo<D>::NCH, CB = Geo<D>::CB;
+    static_assert(Geo<D>::G == 1 && CB == NCH, "refined jobs: d = 2, 3");
+    using MaskT = typename Slot<D>::MaskT;
+    const unsigned lane = lane_id();
+    const TabEntry* te = nullptr;
+    const int nc = setup_common<D, SCHEME_REFINED>(a, S, t, batch, out, te);
+    if (nc <= 0) return out;
+    const uint32_t side = 1u << t.l, msk = side - 1u, S2 = side << 1, msk2 = S2 - 1u;
+    uint32_t Ac[D];
+    morton_decode<D>(t.Cpar, Ac);  // A, level l
+    const uint32_t Cg = t.Cpar >> D;
+    const int eA = (int)(t.Cpar & (uint32_t)(NCH - 1));  // A among its parent's children
+    SETUP_LOOP
+    for (int idx = lane; idx < nc * t.npar; idx += 32) {
+        const int cc = idx / t.npar, q = idx - cc * t.npar;
+        const int e = S.child[cc];
+        const uint32_t P = S.par[q];
+        uint32_t pc[D];
+        morton_decode<D>(P, pc);
+        const int pcmp = P < Cg ? -1 : (P > Cg ? 1 : 0);  // Morton order of B vs A
+        uint32_t cnt[3] = {0u, 0u, 0u}, m[3] = {0u, 0u, 0u};
+#pragma unroll
+        for (int sc = 0; sc < NCH; ++sc) {
+            uint32_t dm = 0, h = 0;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                const uint32_t b = (pc[k] << 1) | (((uint32_t)sc >> (D - 1 - k)) & 1u);  // B, level l
+                const uint32_t df = (b - Ac[k]) & msk;
+                dm = max(dm, min(df, side - df));
+                const uint32_t a2 = (Ac[k] << 1) | (((uint32_t)e >> (D - 1 - k)) & 1u);  // a, level l + 1
+                const uint32_t dd = (2u * b - a2) & msk2;  // B = [dd, dd + 2) relative to a = [0, 1)
+                const uint32_t g = (dd == 0u || dd == S2 - 1u) ? 0u : min(dd - 1u, S2 - dd - 2u);
+                h = max(h, g);
+            }
+            const bool gt = pcmp > 0 || (pcmp == 0 && sc > eA);
+            if (dm <= 1u || !(t.i < t.j || gt)) continue;  // neighbours of A: no type-II event; i == j: B > A (R16)
+            const int kind = h <= 2u ? 0 : (h == 3u ? 1 : 2);
+            const uint32_t nB = S.rstart[q][sc + 1] - S.rstart[q][sc];
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk)
+                if (kk == kind) {
+                    m[kk] |= 1u << sc;
+                    cnt[kk] += nB;
+                }
+        }
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+            S.mask[cc][kk][q] = (MaskT)m[kk];
+            S.pre[cc][kk][q] = cnt[kk];
+        }
+    }
+    __syncwarp();
+    // per (child, class): prefix over parents and the sequence; every sequence is a chain sequence
+    constexpr int NE = (3 * CB + 31) / 32;
+    unsigned long long units[NE];
+#pragma unroll
+    for (int h = 0; h < NE; ++h) {
+        units[h] = 0;
+        const int q3 = (int)lane + 32 * h;
+        if (q3 < nc * 3) {
+            const int cc = q3 / 3, k = q3 - 3 * cc;
+            uint32_t acc = 0;
+            SETUP_LOOP
+            for (int q = 0; q < t.npar; ++q) {
+                const uint32_t c = S.pre[cc][k][q];
+                S.pre[cc][k][q] = acc;
+                acc += c;
+            }
+            S.pre[cc][k][t.npar] = acc;
+            const int e = S.child[cc];
+            Seq& Q = S.seq[cc][k];
+            Q.A = (t.Cpar << D) + (uint32_t)e;  // a on level l + 1: the Philox key of its sequences
+            Q.a0 = S.achild[e];
+            Q.nA = S.achild[e + 1] - Q.a0;
+            Q.M = acc;
+            Q.cl2 = 0;
+            if (acc && S.job.pbar[k] > 0.0) {
+                const unsigned long long N = (unsigned long long)Q.nA * acc;
+                Q.cl2 = chunk_log2(N, S.job.clog2m[k], 32);
+                units[h] = ((N - 1) >> Q.cl2) + 1;
+            }
+        }
+    }
+    unsigned long long base = 0, wk = 0;
+    int n2 = 0;
+#pragma unroll
+    for (int h = 0; h < NE; ++h) {
+        const int q3 = (int)lane + 32 * h;
+        const unsigned long long incl = warp_incl_scan64(units[h]) + base;
+        if (q3 < nc * 3) S.uoff[q3 + 1] = incl;
+        base = shfl64(incl, 31);
+        wk += units[h] * 8ull;
+        n2 += __popc(__ballot_sync(FULL, units[h] != 0));
+    }
+    if (lane == 0) S.uoff[0] = 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) wk += __shfl_xor_sync(FULL, wk, o);
+    out.work = wk;
+    out.U = base;
+    out.nseq2 = n2;
+    __syncwarp();
+    return out;
+}
+
 // d = 1 job setup: one lane per child lists its <= 3 cell ranges per kind directly (offsets
 // -3..3 from the child, or every region cell when the region is the whole level, lg <= 1).
 template <int SCHEME>
@@ -835,7 +971,7 @@ __device__ __noinline__ JobSetup setup_job1(const SampleArgs& a, Slot1& S, const
 {
     JobSetup out = {0ull, 0ull, 0, 0};
     const TabEntry* te = nullptr;
-    const int nc = setup_common<1>(a, S, t, batch, out, te);
+    const int nc = setup_common<1, SCHEME>(a, S, t, batch, out, te);
     if (nc <= 0) return out;
     const unsigned lane = lane_id();
     const int subl = t.cs, nsub = 1 << t.cs;  // d = 1: the shift is the level difference
@@ -948,8 +1084,13 @@ __device__ __noinline__ JobSetup setup_job1(const SampleArgs& a, Slot1& S, const
 template <int D, int SCHEME>
 __device__ __forceinline__ JobSetup setup_any(const SampleArgs& a, SlotT<D>& S, const TaskDesc t, int batch)
 {
-    if constexpr (D == 1) return setup_job1<SCHEME>(a, S, t, batch);
-    else return setup_job<D, SCHEME>(a, S, t, batch);
+    if constexpr (D == 1) {
+        return setup_job1<SCHEME>(a, S, t, batch);
+    } else {
+        if constexpr (SCHEME == SCHEME_REFINED)
+            if (t.ref) return setup_job_ref<D>(a, S, t, batch);
+        return setup_job<D, SCHEME>(a, S, t, batch);
+    }
 }
 
 // d = 1 slot: the range holding concatenated index t of sequence (cc, k)
@@ -1210,7 +1351,9 @@ struct TileSource {
                     task = __ldg(&a.tasks[otoff + (tk - ostart)]);
                 }
                 ++tk;
-                const int lg = max(0, ((task >> 6) & 63) - Geo<D>::G);
+                int lg = max(0, ((task >> 6) & 63) - Geo<D>::G);
+                if constexpr (SCHEME == SCHEME_REFINED)
+                    if ((task >> 14) & 1) lg = (task >> 6) & 63;  // refined job: the task cell is A itself, on level l
                 t = make_task<D>(oi, task, ocode >> (D * (oI - lg)));
                 batch = 0;
 
@@ -1324,6 +1467,8 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
             if (chain) {
                 const SlotT<D>& S = W.slot[ls];
                 const uint32_t A = S.seq[cc][kind].A;
+                if constexpr (SCHEME == SCHEME_REFINED) ctr = make_uint4(A, ch, S.job.tag + ((uint32_t)kind << 17), r);
+                else
                 ctr = SCHEME == SCHEME_MERGED ? make_uint4(A, ch, S.job.tag | ((uint32_t)(kind - 1) << 17) | (1u << 18), r)
                                               : make_uint4(A, Bev, S.job.tag | (ch << 17), r);
             } else {
@@ -1345,15 +1490,16 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
             const Seq& Q = S.seq[cc][kind];
             ++r;
             if (STATS) ++C.draws;
-            const double pb_ = S.job.pbar[kind - 1];
+            constexpr int KO = KOff<SCHEME>::v;
+            const double pb_ = S.job.pbar[kind - KO];
             const double rj = u53(o.x, o.y);
             const long long remaining = end - pos - 1;
             // skip = floor(log(1-rj)/log1p(-pbar)) (R10): fast float path, canonical double fallback
             long long skip = 0;
             int st = (pb_ == 1.0 || rj == 0.0) ? (remaining <= 0 ? 1 : 0)  // z = 0 exactly
-                                               : fast_jump(__dsub_rn(1.0, rj), S.job.il2[kind - 1], remaining, skip);
+                                               : fast_jump(__dsub_rn(1.0, rj), S.job.il2[kind - KO], remaining, skip);
             if (STATS || st < 0) {
-                const double z = pb_ == 1.0 ? 0.0 : exact_skip(rj, S.job.Lbar[kind - 1]);
+                const double z = pb_ == 1.0 ? 0.0 : exact_skip(rj, S.job.Lbar[kind - KO]);
                 const int st2 = z >= (double)remaining ? 1 : 0;
                 if (STATS) {
                     if (st < 0) ++C.fb;
@@ -1370,18 +1516,18 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
             } else {
                 pos += 1 + skip;
                 if (STATS) ++C.landings;
-                nk = kind;
+                nk = SCHEME == SCHEME_REFINED ? kind + 1 : kind;  // > 0: a landing (a refined job's kind 0 is a chain)
                 nra = u53(o.z, o.w);
                 npbar = pb_;
                 if constexpr (Src::unified_lookup) {
-                    lpack = (ls << 8) | (cc << 2) | kind;
+                    lpack = (ls << 8) | (cc << 2) | kind | (SCHEME == SCHEME_REFINED ? 128 : 0);  // bit 7: landing
                     lval = (unsigned long long)pos;
                 } else {
                     const unsigned long long g = (unsigned long long)pos;
                     uint32_t ti;
-                    const uint32_t si = divmod(g, SCHEME == SCHEME_MERGED ? Q.M : enB, ti);
+                    const uint32_t si = divmod(g, SCHEME != SCHEME_EVENT ? Q.M : enB, ti);
                     npa = Q.a0 + si;
-                    if (SCHEME == SCHEME_MERGED) {
+                    if (SCHEME != SCHEME_EVENT) {
                         uint32_t B;
                         npb = locate(S, S.job.npar, S.job.cs, cc, kind, ti, B);
                     } else {
@@ -1460,7 +1606,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                 const int qc = q / 3, qk = q - 3 * qc;
                 const Seq& Q = S.seq[qc][qk];
                 const unsigned long long x = u - S.uoff[q];
-                if (qk == 0) {
+                if (qk == 0 && !(SCHEME == SCHEME_REFINED && S.job.ref)) {
                     if constexpr (Src::unified_lookup) {
                         lpack = (ds << 8) | (qc << 2);
                         lval = x;
@@ -1478,7 +1624,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
                     cc = qc;
                     kind = qk;
                     r = 0;
-                    if (SCHEME == SCHEME_MERGED) {
+                    if (SCHEME != SCHEME_EVENT) {
                         ch = (uint32_t)x;
                         const unsigned long long st = x << Q.cl2;
                         pos = (long long)st - 1;
@@ -1504,7 +1650,8 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
         }
         // ---- the lookup: row-major index -> (row s, column t) -> sorted positions ----
         if (Src::unified_lookup && lpack >= 0) {
-            const int lk = lpack & 3, lc = (lpack >> 2) & 63;
+            const int lk = lpack & 3, lc = (lpack >> 2) & 15;
+            const bool cand1 = lk == 0 && !(SCHEME == SCHEME_REFINED && (lpack & 128));  // a dispatched type-I candidate
             const SlotT<D>& S = W.slot[lpack >> 8];
             const Seq& Q = S.seq[lc][lk];
             const bool ev = SCHEME == SCHEME_EVENT && lk > 0;  // EVENT landing: one cell (enB, eb0)
@@ -1516,7 +1663,7 @@ __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src&
             } else {
                 uint32_t B;
                 npb = locate(S, S.job.npar, S.job.cs, lc, lk, ti, B);
-                if (lk == 0 && !(S.job.same_layer && B == Q.A && npb <= npa)) nk = 0;  // same cell: only s < t (R16)
+                if (cand1 && !(S.job.same_layer && B == Q.A && npb <= npa)) nk = 0;  // same cell: only s < t (R16)
             }
         }
         // ---- (5) issue the loads of the next candidate ----

@@ -1,0 +1,94 @@
+"""GPU parity of GIRG_SCHEME_REFINED (R27: the refined type-II bound, SURVEY 8(f)
+NEXT-1(b)) against the oracle's REFINED scheme, element by element, through the C ABI.
+
+Each case runs the production kernels (stats=False) and the counting build (stats=True), with the
+level rule at its default (>= 8 points of layer i per level-l cell), forced onto every level
+l < CL(i,j) (ref_x = -1: refined sequences at small n) and at an intermediate threshold; the
+oracle's and the device's near-tie counters must be zero, and the work counters (draws, landings,
+accepted edges) equal.  REFINED must also do strictly less type-II work than MERGED where it
+applies, and be MERGED where it does not (d = 1, T = 0).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from workloads import BY_NAME, synth_inputs
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1905_06706_b200 as girg  # noqa: E402
+
+from test_gpu_parity import assert_parity, dev, gpu_keys  # noqa: E402
+
+
+@pytest.fixture
+def ref_x():
+    """Sets the REFINED level threshold on both sides; restores the default afterwards."""
+
+    def set_both(x):
+        O.set_ref_x(x)
+        girg.debug_set_ref_x(x)
+
+    yield set_both
+    set_both(0)
+
+
+@pytest.mark.parametrize("x", [0, -1, 2], ids=["default", "all-levels", "x2"])
+@pytest.mark.parametrize("d,T,beta,n,deg", [(2, 0.8, 2.2, 6007, 12.0), (3, 0.9, 2.9, 9001, 20.0),
+                                             (2, 0.3, 3.0, 40_000, 8.0), (3, 0.5, 2.5, 50_000, 10.0),
+                                             (3, 0.9, 2.9, 300_000, 20.0)])
+def test_refined_parity(d, T, beta, n, deg, x, ref_x):
+    ref_x(x)
+    w, xs = synth_inputs(n, d, beta, 17 * d + n % 13)
+    kappa = O.scale_weights(w, deg, d, T, beta)
+    g, st, so = assert_parity(w, xs, d, T, kappa, 5 + d, scheme=girg.SCHEME_REFINED)
+    assert st["chunks"] == so["chunks"]
+    if x == -1:  # every level below CL refined: the refined sequences carry work
+        assert so["landings"] > 0
+
+
+def test_refined_less_work_than_merged_same_type1(ref_x):
+    """Same candidate pairs and type-I work as MERGED; fewer landings and draws (the tighter bound)."""
+    ref_x(0)
+    c = BY_NAME["C3"]
+    n = 400_000
+    w, xs = synth_inputs(n, c.d, c.beta, c.seed)
+    kappa = O.scale_weights(w, c.avg_deg, c.d, c.T, c.beta)
+    wd, xd = dev(w), dev(xs)
+    _, sm = girg.edges(wd, xd, c.T, kappa, 3, stats=True, scheme=girg.SCHEME_MERGED)
+    _, sr = girg.edges(wd, xd, c.T, kappa, 3, stats=True, scheme=girg.SCHEME_REFINED)
+    assert sr["cand1"] == sm["cand1"] and sr["edges1"] == sm["edges1"]  # type-I is pair-keyed (R17)
+    assert sr["landings"] < sm["landings"] and sr["draws"] < sm["draws"], (sr, sm)
+
+
+@pytest.mark.parametrize("d,T", [(1, 0.5), (2, 0.0), (4, 0.6)])
+def test_refined_is_merged_where_it_does_not_apply(d, T, ref_x):
+    ref_x(-1)
+    w, xs = synth_inputs(20_000, d, 2.5, 40 + d)
+    kappa = O.scale_weights(w, 10.0, d, T, 2.5)
+    wd, xd = dev(w), dev(xs)
+    em = girg.edges(wd, xd, T, kappa, 9, scheme=girg.SCHEME_MERGED)
+    er = girg.edges(wd, xd, T, kappa, 9, scheme=girg.SCHEME_REFINED)
+    assert np.array_equal(gpu_keys(em), gpu_keys(er))
+    eo, _ = O.edges(w, xs, d, T, kappa, 9, with_stats=True, scheme=O.SCHEME_REFINED)
+    assert np.array_equal(gpu_keys(er), O.sort_edges(eo))
+
+
+def test_refined_sharded_union(ref_x):
+    """Ranked (interleaved) shards of a REFINED run partition its edge set, and each equals the
+    oracle's shard."""
+    ref_x(-1)
+    d, T, n = 3, 0.7, 30_000
+    w, xs = synth_inputs(n, d, 2.6, 77)
+    kappa = O.scale_weights(w, 12.0, d, T, 2.6)
+    full, _, _ = assert_parity(w, xs, d, T, kappa, 4, scheme=girg.SCHEME_REFINED)
+    parts = []
+    for r in range(3):
+        g, _, _ = assert_parity(w, xs, d, T, kappa, 4, shard=("ranked", 2, 3, r), scheme=girg.SCHEME_REFINED)
+        parts.append(g)
+    u = np.sort(np.concatenate(parts))
+    assert np.array_equal(u, full)
