@@ -133,7 +133,7 @@ int girg_edges_shard(const double *w_dev, const double *x_dev, uint64_t n, int d
                                 P:494-501), chunks of 2..4 expected landings */
 #define GIRG_SCHEME_REFINED 2 /* MERGED with the refined bound of DESIGN.md R27 (P:486-491 with a
                                 tighter minimum distance) where it pays: for d = 2, 3, T > 0, on the
-                                levels l < CL(i,j) with >= 8 points of layer i per cell, the rows of
+                                levels l < CL(i,j) with >= 4096 points of layer i per cell, the rows of
                                 an A cell are split by A's children on level l+1 and its distant
                                 cells classed by their box distance from the child (2, 3, >= 4
                                 half-cells), one sequence per (child, class).  Elsewhere (and for
@@ -265,7 +265,7 @@ const char *girg_last_cuda_error(void);
 int girg_version(void);
 
 /* TEST HOOK (not part of the product API): threshold of GIRG_SCHEME_REFINED's level rule, in
- * points of layer i per level-l cell: 0 = the default (8), k > 0 = k points, -1 = every level
+ * points of layer i per level-l cell: 0 = the default (4096), k > 0 = k points, -1 = every level
  * l < CL(i,j), so that small parity cases exercise refined sequences.  Process-wide.  Returns 0. */
 int girg_debug_set_ref_x(int x);
 

@@ -336,7 +336,7 @@ def set_tie_hook(mode: int, delta: float = 0.0):
 
 
 def set_ref_x(x: int):
-    """TEST HOOK (R27 pins at small n): REFINED threshold, 0 = default (8 points per cell),
+    """TEST HOOK (R27 pins at small n): REFINED threshold, 0 = default (4096 points per cell),
     k > 0 = k points, -1 = every level l < CL(i,j)."""
     lib().or_set_ref_x(int(x))
 

@@ -778,7 +778,7 @@ static void type2_merged(or_ctx *c, int l, uint32_t A, int i, int j, int k, cons
  * 2^-(l+1); a pair (u in a, v in B) is at distance >= h 2^-(l+1) (P:486-491 with a tighter
  * mind).  Classes k = 0, 1, 2 for h = 2, 3, >= 4 (bound taken at h = 2, 3, 4).  Applied where
  * ref_level() says (R27). */
-#define OR_REF_X 8 /* R27: refine a level when layer i has >= 8 points per level-l cell on average */
+#define OR_REF_X 4096 /* R27: refine a level when layer i has >= 4096 points per level-l cell on average (R27) */
 static int or_ref_x = 0;  /* TEST HOOK: 0 = OR_REF_X, k > 0 = k points, -1 = every level l < CL */
 void or_set_ref_x(int x) { or_ref_x = x; }
 

@@ -90,7 +90,7 @@ void or_set_tie_hook(int mode, double delta);
  * the same bound concatenated (R22, exact in distribution; the product default). */
 #define OR_SCHEME_EVENT 0
 #define OR_SCHEME_MERGED 1
-/* REFINED = MERGED, except on the levels l < CL(i,j) where layer i has >= 8 points per level-l
+/* REFINED = MERGED, except on the levels l < CL(i,j) where layer i has >= 4096 points per level-l
  * cell on average (d = 2, 3): there the rows of A are split by A's children on level l+1 and the
  * distant cells classed by their box distance from the child (R27) */
 #define OR_SCHEME_REFINED 2

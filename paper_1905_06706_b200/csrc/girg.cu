@@ -711,7 +711,7 @@ struct HostPlan {
 // R27 (refined type-II bound): level l of layer pair (i, j) is refined where it pays -- d = 2, 3,
 // T > 0, l < CL(i,j) (no type-I events on that level, and l + 1 <= I(i)) and at least REF_X points
 // of layer i per level-l cell on average (R27; the oracle's ref_level()).
-constexpr long REF_X = 8;
+constexpr long REF_X = 4096;  // B200 sweep optimum (profiles/r02/refined/): 1024..16384 within 1 %, 8 is 40 % slower
 static std::atomic<int> g_ref_x{0};  // TEST HOOK (girg_debug_set_ref_x): 0 = REF_X, k > 0 = k points, -1 = every l < CL
 static bool ref_level(int scheme, int d, double T, int l, int cl, uint64_t cnt_i)
 {

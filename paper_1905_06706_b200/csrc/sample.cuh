@@ -881,29 +881,43 @@ __device__ __noinline__ JobSetup setup_job_ref(const SampleArgs& a, Slot<D>& S, 
         morton_decode<D>(P, pc);
         const int pcmp = P < Cg ? -1 : (P > Cg ? 1 : 0);  // Morton order of B vs A
         uint32_t cnt[3] = {0u, 0u, 0u}, m[3] = {0u, 0u, 0u};
+        // Sub-cell sets as bit masks, separable per dimension (as setup_job's MERGED path): nb =
+        // neighbours of A, le2 / le3 = half-cell gap from a <= 2 / <= 3 (neighbours of A lie in le2)
+        constexpr uint32_t FULLN = (1u << NCH) - 1u;
+        uint32_t nb = FULLN, le2 = FULLN, le3 = FULLN;
 #pragma unroll
-        for (int sc = 0; sc < NCH; ++sc) {
-            uint32_t dm = 0, h = 0;
+        for (int k = 0; k < D; ++k) {
+            uint32_t p1 = 0u;
 #pragma unroll
-            for (int k = 0; k < D; ++k) {
-                const uint32_t b = (pc[k] << 1) | (((uint32_t)sc >> (D - 1 - k)) & 1u);  // B, level l
+            for (int sc = 0; sc < NCH; ++sc) p1 |= ((sc >> (D - 1 - k)) & 1) ? (1u << sc) : 0u;
+            const uint32_t p0 = FULLN ^ p1;
+            const uint32_t a2 = (Ac[k] << 1) | (((uint32_t)e >> (D - 1 - k)) & 1u);  // a, level l + 1
+            uint32_t sel_nb = 0u, sel2 = 0u, sel3 = 0u;
+#pragma unroll
+            for (int bit = 0; bit < 2; ++bit) {
+                const uint32_t b = (pc[k] << 1) | (uint32_t)bit;  // B, level l
                 const uint32_t df = (b - Ac[k]) & msk;
-                dm = max(dm, min(df, side - df));
-                const uint32_t a2 = (Ac[k] << 1) | (((uint32_t)e >> (D - 1 - k)) & 1u);  // a, level l + 1
                 const uint32_t dd = (2u * b - a2) & msk2;  // B = [dd, dd + 2) relative to a = [0, 1)
                 const uint32_t g = (dd == 0u || dd == S2 - 1u) ? 0u : min(dd - 1u, S2 - dd - 2u);
-                h = max(h, g);
+                const uint32_t pm = bit ? p1 : p0;
+                sel_nb |= min(df, side - df) <= 1u ? pm : 0u;
+                sel2 |= g <= 2u ? pm : 0u;
+                sel3 |= g <= 3u ? pm : 0u;
             }
-            const bool gt = pcmp > 0 || (pcmp == 0 && sc > eA);
-            if (dm <= 1u || !(t.i < t.j || gt)) continue;  // neighbours of A: no type-II event; i == j: B > A (R16)
-            const int kind = h <= 2u ? 0 : (h == 3u ? 1 : 2);
+            nb &= sel_nb;
+            le2 &= sel2;
+            le3 &= sel3;
+        }
+        uint32_t GT = FULLN;  // i == j: only B > A (R16)
+        if (!(t.i < t.j || pcmp > 0)) GT = pcmp < 0 ? 0u : (FULLN << (eA + 1)) & FULLN;
+        m[0] = le2 & ~nb & GT;
+        m[1] = le3 & ~le2 & GT;
+        m[2] = ~le3 & GT & FULLN;
+#pragma unroll
+        for (int sc = 0; sc < NCH; ++sc) {
             const uint32_t nB = S.rstart[q][sc + 1] - S.rstart[q][sc];
 #pragma unroll
-            for (int kk = 0; kk < 3; ++kk)
-                if (kk == kind) {
-                    m[kk] |= 1u << sc;
-                    cnt[kk] += nB;
-                }
+            for (int kk = 0; kk < 3; ++kk) cnt[kk] += ((m[kk] >> sc) & 1u) ? nB : 0u;
         }
 #pragma unroll
         for (int kk = 0; kk < 3; ++kk) {
@@ -1429,6 +1443,7 @@ struct ItemSource {
 template <int D, int SCHEME, bool STATS, class Src>
 __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src& src, Counters& C)
 {
+    static_assert(Geo<D>::CB <= 16, "the lookup pack holds the child in 4 bits");
     const unsigned lane = lane_id();
     const bool T0 = a.T == 0.0;
     const double s_ = a.s, invT = a.invT;

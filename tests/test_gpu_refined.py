@@ -2,8 +2,8 @@
 NEXT-1(b)) against the oracle's REFINED scheme, element by element, through the C ABI.
 
 Each case runs the production kernels (stats=False) and the counting build (stats=True), with the
-level rule at its default (>= 8 points of layer i per level-l cell), forced onto every level
-l < CL(i,j) (ref_x = -1: refined sequences at small n) and at an intermediate threshold; the
+level rule at its default (>= 4096 points of layer i per level-l cell), forced onto every level
+l < CL(i,j) (ref_x = -1: refined sequences at small n) and at intermediate thresholds (2, 8); the
 oracle's and the device's near-tie counters must be zero, and the work counters (draws, landings,
 accepted edges) equal.  REFINED must also do strictly less type-II work than MERGED where it
 applies, and be MERGED where it does not (d = 1, T = 0).
@@ -37,7 +37,7 @@ def ref_x():
     set_both(0)
 
 
-@pytest.mark.parametrize("x", [0, -1, 2], ids=["default", "all-levels", "x2"])
+@pytest.mark.parametrize("x", [0, -1, 2, 8], ids=["default", "all-levels", "x2", "x8"])
 @pytest.mark.parametrize("d,T,beta,n,deg", [(2, 0.8, 2.2, 6007, 12.0), (3, 0.9, 2.9, 9001, 20.0),
                                              (2, 0.3, 3.0, 40_000, 8.0), (3, 0.5, 2.5, 50_000, 10.0),
                                              (3, 0.9, 2.9, 300_000, 20.0)])
@@ -53,7 +53,7 @@ def test_refined_parity(d, T, beta, n, deg, x, ref_x):
 
 def test_refined_less_work_than_merged_same_type1(ref_x):
     """Same candidate pairs and type-I work as MERGED; fewer landings and draws (the tighter bound)."""
-    ref_x(0)
+    ref_x(8)
     c = BY_NAME["C3"]
     n = 400_000
     w, xs = synth_inputs(n, c.d, c.beta, c.seed)
@@ -92,3 +92,52 @@ def test_refined_sharded_union(ref_x):
         parts.append(g)
     u = np.sort(np.concatenate(parts))
     assert np.array_equal(u, full)
+
+
+def test_C3_full_refined_parity(ref_x):
+    """BASELINE config 3 (n = 10^6, d = 2) in full with the default level rule."""
+    ref_x(0)
+    c = BY_NAME["C3"]
+    w, xs = synth_inputs(c.n, c.d, c.beta, c.seed)
+    kappa = O.scale_weights(w, c.avg_deg, c.d, c.T, c.beta)
+    g, st, so = assert_parity(w, xs, c.d, c.T, kappa, c.seed, scheme=girg.SCHEME_REFINED)
+    assert abs(2 * len(g) / c.n - c.avg_deg) < 0.01 * c.avg_deg
+    _, sm = O.edges(w, xs, c.d, c.T, kappa, c.seed, with_stats=True, scheme=O.SCHEME_MERGED)
+    assert so["landings"] < sm["landings"]  # refined levels exist at this size
+
+
+def test_C5_refined_sampled_shard_parity(ref_x):
+    """BASELINE config 5 (n = 2^24, d = 3) with the default level rule, in the launch configuration
+    the bench times with --scheme refined: sampled level-3 shards (a corner block, which owns the
+    coarse events of its ancestors, and two interior ones) equal the oracle's, and each is a subset
+    of the full REFINED edge set.  kappa is the oracle's (tests/golden/oracle_kappa.json)."""
+    import json
+    import os
+
+    from test_gpu_parity import assert_device_clean, run_both
+
+    ref_x(0)
+    c = BY_NAME["C5"]
+    w, xs = synth_inputs(c.n, c.d, c.beta, c.seed)
+    with open(os.path.join(os.path.dirname(__file__), "golden", "oracle_kappa.json")) as f:
+        kappa = json.load(f)["C5"]
+    wd, xd = dev(w), dev(xs)
+    full, st = girg.edges(wd, xd, c.T, kappa, c.seed, stats=True, scheme=girg.SCHEME_REFINED)
+    m = full.shape[0]
+    assert abs(2 * m / c.n - c.avg_deg) < 0.01 * c.avg_deg
+    # jump near-ties are a diagnostic (R21 / R26; test_C5_full_parity_all_shards[refined] compares
+    # their count with the oracle's over the whole graph)
+    assert st["neartie1"] == st["neartie2"] == st["fast_mismatch"] == 0 and st["neartie_jump"] <= 2, st
+    _, sm = girg.edges(wd, xd, c.T, kappa, c.seed, stats=True, scheme=girg.SCHEME_MERGED)
+    assert st["landings"] < sm["landings"] and st["cand1"] == sm["cand1"] and st["edges1"] == sm["edges1"]
+    k = girg.edge_keys(full)
+    assert bool((k[1:] != k[:-1]).all())
+    for lo, hi in ((0, 1), (200, 201), (363, 364)):
+        g, o, stg, so, gp = run_both(w, xs, c.d, c.T, kappa, c.seed, shard=(3, lo, hi), scheme=girg.SCHEME_REFINED)
+        assert so["nt1"] + so["nt2acc"] == 0 and so["nt2jump"] == stg["neartie_jump"], (so, stg)
+        assert np.array_equal(g, o) and np.array_equal(gp, o)
+        assert stg["neartie1"] == stg["neartie2"] == stg["fast_mismatch"] == 0, stg
+        assert stg["landings"] == so["landings"] and stg["draws"] == so["draws"]
+        gd = torch.from_numpy(g.astype(np.int64)).cuda()
+        pos = torch.searchsorted(k, gd).clamp(max=m - 1)
+        assert bool((k[pos] == gd).all())

@@ -41,7 +41,7 @@ def test_threshold_C1_full_bruteforce(oracle):
 
 
 # "refined_all": R27 on every level l < CL(i,j) (the ref_x test hook), so that the small pin
-# graphs exercise the refined sequences, which the default threshold (8 points per cell) only
+# graphs exercise the refined sequences, which the default threshold (4096 points per cell) only
 # reaches at larger n
 SCHEMES = pytest.mark.parametrize("scheme", [0, 1, 2, "refined_all"], ids=["event", "merged", "refined", "refined_all"],
                                   indirect=True)
@@ -183,14 +183,18 @@ def test_merged_scheme_reduces_draws(oracle):
 @pytest.mark.parametrize("d,T,beta,deg", [(3, 0.9, 2.9, 20.0), (2, 0.8, 2.2, 20.0)])
 def test_refined_scheme_cuts_landings(oracle, d, T, beta, deg):
     """R27: the same candidate pairs and type-I work as R22; on the refined
-    levels (l < CL(i,j), >= 8 points of layer i per cell) sequences per (child of A, distance
+    levels (l < CL(i,j), here >= 8 points of layer i per cell) sequences per (child of A, distance
     class) instead of per (A, delta_max), and markedly fewer landings for the same edges in
     expectation (the bound of a far child is (2/3)^(d/T) of A's)."""
     n = 60000
     w, x = synth_inputs(n, d, beta, 5)
     kappa = oracle.scale_weights(w, deg, d, T, beta)
     em, sm = oracle.edges(w, x, d, T, kappa, 3, with_stats=True, scheme=1)
-    er, sr = oracle.edges(w, x, d, T, kappa, 3, with_stats=True, scheme=2)
+    oracle.set_ref_x(8)  # the level rule at 8 points per cell (the default, 4096, refines nothing at this n)
+    try:
+        er, sr = oracle.edges(w, x, d, T, kappa, 3, with_stats=True, scheme=2)
+    finally:
+        oracle.set_ref_x(0)
     assert sm["cand1"] == sr["cand1"] and sm["acc1"] == sr["acc1"]
     assert sm["cand2"] == sr["cand2"]
     assert sr["ev2_nonempty"] > 1.4 * sm["ev2_nonempty"]  # the children's sequences exist
