@@ -269,6 +269,17 @@ int girg_version(void);
  * l < CL(i,j), so that small parity cases exercise refined sequences.  Process-wide.  Returns 0. */
 int girg_debug_set_ref_x(int x);
 
+/* TEST HOOK (not part of the product API): the Lemma-1 index that girg_edges builds for these
+ * inputs (App. A; H5), for a direct comparison with the oracle's:
+ * sid_dev[n] (device) = vertex ids in sorted order (by layer, then Morton cell on level I(layer),
+ * then id); P_dev[min(K+1, P_cap)] (device) = first sorted position of every cell of the
+ * concatenated cell space (layer i's 2^(d I(i)) cells start at base[i]; P[K] = n).  Host outputs:
+ * *K_out, *L_out (layers), base_out[L+1], lstart_out[L+1], I_out[L] (arrays of 65 / 65 / 64).
+ * Either device pointer may be NULL.  Runs the whole pipeline with edge capacity 0.  Synchronises. */
+int girg_debug_index(const double *w_dev, const double *x_dev, uint64_t n, int d, double T, double kappa,
+                     uint32_t *sid_dev, uint32_t *P_dev, uint64_t P_cap, uint64_t *K_out, int *L_out,
+                     uint32_t *base_out, uint32_t *lstart_out, uint8_t *I_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,13 +74,16 @@ _lib.girg_strerror.restype = C.c_char_p
 _lib.girg_last_cuda_error.restype = C.c_char_p
 for _f in ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
            "girg_edges_ex", "girg_edges_host", "girg_edges_batch", "girg_version", "girg_last_timings",
-           "girg_hrg_points", "girg_hrg_edges", "girg_debug_set_ref_x"):
+           "girg_hrg_points", "girg_hrg_edges", "girg_debug_set_ref_x", "girg_debug_index"):
     getattr(_lib, _f).restype = C.c_int
 _lib.girg_debug_set_ref_x.argtypes = [_i]
+_lib.girg_debug_index.argtypes = [_vp, _vp, _u64, _i, _d, _d, _vp, _vp, _u64, C.POINTER(_u64), C.POINTER(_i), _vp, _vp,
+                                  _vp, _vp]
 
 EXPORTS = ("girg_weights", "girg_positions", "girg_scale_weights", "girg_edges", "girg_edges_shard",
            "girg_edges_ex", "girg_edges_host", "girg_edges_batch", "girg_strerror", "girg_last_cuda_error", "girg_version",
-           "girg_last_timings", "girg_hrg_points", "girg_hrg_edges", "girg_debug_set_ref_x")
+           "girg_last_timings", "girg_hrg_points", "girg_hrg_edges", "girg_debug_set_ref_x",
+           "girg_debug_index")
 
 
 class GirgError(RuntimeError):
@@ -129,6 +132,30 @@ def library_path() -> str:
 
 def version() -> int:
     return _lib.girg_version()
+
+
+def debug_index(w: torch.Tensor, x: torch.Tensor, T: float, kappa: float, stream=None):
+    """TEST HOOK (include/girg.h girg_debug_index): the Lemma-1 index of a girg_edges call as
+    (sid [n] int32 view of uint32, P [K+1], base [L+1], lstart [L+1], I [L])."""
+    import numpy as np
+
+    _dev_f64(w, "w")
+    _dev_f64(x, "x")
+    n = w.numel()
+    d = x.numel() // n
+    base = np.zeros(65, dtype=np.uint32)
+    lstart = np.zeros(65, dtype=np.uint32)
+    Il = np.zeros(64, dtype=np.uint8)
+    K, L = _u64(0), _i(0)
+    with torch.cuda.device(w.device):
+        sid = torch.empty(n, dtype=torch.int32, device=w.device)
+        _check(_lib.girg_debug_index(w.data_ptr(), x.data_ptr(), n, d, T, kappa, sid.data_ptr(), None, 0, C.byref(K),
+                                     C.byref(L), base.ctypes.data, lstart.ctypes.data, Il.ctypes.data, _stream(stream)))
+        P = torch.empty(K.value + 1, dtype=torch.int32, device=w.device)
+        _check(_lib.girg_debug_index(w.data_ptr(), x.data_ptr(), n, d, T, kappa, None, P.data_ptr(), K.value + 1,
+                                     C.byref(K), C.byref(L), base.ctypes.data, lstart.ctypes.data, Il.ctypes.data,
+                                     _stream(stream)))
+    return sid, P, base[: L.value + 1].copy(), lstart[: L.value + 1].copy(), Il[: L.value].copy()
 
 
 def debug_set_ref_x(x: int) -> None:

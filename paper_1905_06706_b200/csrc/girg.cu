@@ -1051,6 +1051,10 @@ struct EdgeCall {
     HostPlan hp;
     SampleArgs a;
     char* misc = nullptr;  // device status block (err, m, counters, queue counters)
+    // TEST HOOK (girg_debug_index): device buffers that receive the sorted ids and the prefix array
+    uint32_t* dbg_sid = nullptr;
+    uint32_t* dbg_P = nullptr;
+    uint64_t dbg_Pcap = 0;
     char* hmisc = nullptr;
     char hmisc_local[256];
     unsigned nb = 0;
@@ -1169,6 +1173,10 @@ struct EdgeCall {
             case 4: launch_index<4>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, big, nbig, d_err, st); break;
             default: launch_index<5>(w, x, n32, d_plan, K, key, cnt, P, bsum, tk, inv, sid, skey, rec, big, nbig, d_err, st); break;
         }
+        if (dbg_sid) GCHECK(cudaMemcpyAsync(dbg_sid, sid, n * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        if (dbg_P)
+            GCHECK(cudaMemcpyAsync(dbg_P, P, std::min<uint64_t>(K + 1, dbg_Pcap) * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToDevice, st));
         a.pl = d_plan;
         a.tab = d_tab;
         a.tasks = d_tasks;
@@ -2329,6 +2337,47 @@ extern "C" int girg_last_timings(girg_timings* out)
 extern "C" const char* girg_last_cuda_error(void) { return girg::g_last_cuda.c_str(); }
 
 extern "C" int girg_version(void) { return 201; }
+extern "C" int girg_debug_index(const double* w_dev, const double* x_dev, uint64_t n, int d, double T, double kappa,
+                                uint32_t* sid_dev, uint32_t* P_dev, uint64_t P_cap, uint64_t* K_out, int* L_out,
+                                uint32_t* base_out, uint32_t* lstart_out, uint8_t* I_out, void* stream)
+{
+    using namespace girg;
+    uint64_t m = 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    int v = EdgeCall::validate(w_dev, x_dev, n, d, T, kappa, 0, 0, 1, SCHEME_MERGED, nullptr, 0, &m);
+    if (v != GIRG_OK) return v;
+    if (!K_out || !L_out || !base_out || !lstart_out || !I_out) return GIRG_EINVAL;
+    try {
+        EdgeCall E(w_dev, x_dev, n, d, T, kappa, 0, 0, 0, 1, SCHEME_MERGED, nullptr, 0, &m, nullptr, st);
+        E.dbg_sid = sid_dev;
+        E.dbg_P = P_dev;
+        E.dbg_Pcap = P_cap;
+        E.stage_a();
+        GCHECK(cudaStreamSynchronize(st));
+        E.stage_b();
+        if (E.rc != GIRG_OK) return E.rc;
+        GCHECK(cudaStreamSynchronize(st));
+        const int rc = E.stage_c();  // the sampler ran with capacity 0: ECAPACITY is the expected outcome
+        if (rc != GIRG_OK && rc != GIRG_ECAPACITY) return rc;
+        const Plan& p = E.hp.p;
+        *K_out = E.hp.K;
+        *L_out = p.L;
+        for (int i = 0; i <= p.L; ++i) {
+            base_out[i] = p.base[i];
+            lstart_out[i] = p.lstart[i];
+        }
+        for (int i = 0; i < p.L; ++i) I_out[i] = p.I[i];
+        return GIRG_OK;
+    } catch (const CudaFail& f) {
+        return map_cuda(f.e);
+    } catch (const std::bad_alloc&) {
+        return GIRG_ENOMEM;
+    } catch (...) {
+        g_last_cuda = "internal error: unexpected exception";
+        return GIRG_ECUDA;
+    }
+}
+
 extern "C" int girg_debug_set_ref_x(int x)
 {
     girg::g_ref_x.store(x);

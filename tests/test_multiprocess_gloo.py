@@ -91,7 +91,7 @@ def test_shard_ranges_partition_blocks():
             assert (1 << (d * sl)) >= 4096 * world or d * (sl + 1) > 30
 
 
-@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("scheme", [0, 1, 2])
 def test_ranked_shards_partition_and_spread_coarse_events(scheme):
     """Interleaved ownership (SURVEY 8(e) "Balance"), oracle only: for N = 3 and 4 the shards are
     disjoint, their union is the full edge set, and no rank is starved or overloaded -- the
@@ -106,11 +106,16 @@ def test_ranked_shards_partition_and_spread_coarse_events(scheme):
     n, d, T = 8000, 2, 0.7
     w, x = synth_inputs(n, d, 2.3, 17)
     kappa = oracle.scale_weights(w, 12.0, d, T, 2.3)
-    full = oracle.sort_edges(oracle.edges(w, x, d, T, kappa, 5, scheme=scheme))
-    for world in (3, 4):
-        parts = [oracle.sort_edges(oracle.edges(w, x, d, T, kappa, 5, shard=shard_for_rank(d, world, r),
-                                                scheme=scheme)) for r in range(world)]
-        union = np.sort(np.concatenate(parts))
-        assert np.array_equal(union, full)
-        sizes = [len(p) for p in parts]
-        assert max(sizes) < 1.25 * min(sizes), sizes
+    if scheme == 2:
+        oracle.set_ref_x(-1)  # REFINED (R27) on every level below CL: refined jobs are owned by their A cell too
+    try:
+        full = oracle.sort_edges(oracle.edges(w, x, d, T, kappa, 5, scheme=scheme))
+        for world in (3, 4):
+            parts = [oracle.sort_edges(oracle.edges(w, x, d, T, kappa, 5, shard=shard_for_rank(d, world, r),
+                                                    scheme=scheme)) for r in range(world)]
+            union = np.sort(np.concatenate(parts))
+            assert np.array_equal(union, full)
+            sizes = [len(p) for p in parts]
+            assert max(sizes) < 1.25 * min(sizes), sizes
+    finally:
+        oracle.set_ref_x(0)
