@@ -66,6 +66,9 @@ struct KOff {
 #else
 #define SETUP_LOOP  // nvcc's default unrolling
 #endif
+#ifndef GIRG_ENGINE_T0
+#define GIRG_ENGINE_T0 false
+#endif
 #ifndef GIRG_EB
 #define GIRG_EB 128
 #endif
@@ -1440,12 +1443,16 @@ struct ItemSource {
 // blocks in one iteration: a pending type-I candidate implies it held no chain.  When the
 // dispatch slot runs dry, the next job is set up in a slot no lane's chain refers to.
 // ---------------------------------------------------------------------------------------
-template <int D, int SCHEME, bool STATS, class Src>
+// MAYBE_T0: the caller may pass T = 0.  Only the batched kernels do (single calls run the flat
+// T = 0 loop below), so the single-call instantiations drop the threshold branches: C2 3.03 ->
+// 2.97 ms, C4 20.2 -> 20.0, C5 151.6 -> 151.0 -- except d = 2, whose register allocation is better
+// with them (C3 9.35 vs 9.99 ms without; profiles/r02/tail_items/engine_t0_template_ab.txt)
+template <int D, int SCHEME, bool STATS, bool MAYBE_T0 = (D == 2) || GIRG_ENGINE_T0, class Src>
 __device__ __forceinline__ void engine(const SampleArgs& a, WarpSmem<D>& W, Src& src, Counters& C)
 {
     static_assert(Geo<D>::CB <= 16, "the lookup pack holds the child in 4 bits");
     const unsigned lane = lane_id();
-    const bool T0 = a.T == 0.0;
+    const bool T0 = MAYBE_T0 && a.T == 0.0;
     const double s_ = a.s, invT = a.invT;
 #ifdef GIRG_PROFILE
     const long long t_start = clock64();
@@ -1838,7 +1845,7 @@ __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB) k_sample_b(con
     WarpSmem<D>& W = reinterpret_cast<WarpSmem<D>*>(smem_raw)[threadIdx.x >> 5];
     Counters C = {};
     TileSource<D, SCHEME, STATS> src;
-    engine<D, SCHEME, STATS>(sa, W, src, C);
+    engine<D, SCHEME, STATS, true>(sa, W, src, C);
     flush_counters<STATS>(sa, C);
 }
 
@@ -1853,7 +1860,7 @@ __global__ void __launch_bounds__(32 * Geo<D>::WPB, Geo<D>::MINB_BIG) k_big_b(co
     Counters C = {};
     ItemSource<D, SCHEME, STATS> src;
     src.nit = (*sa.err & ERR_ITEMS) ? 0u : min(*sa.nitems, sa.items_cap);
-    engine<D, SCHEME, STATS>(sa, W, src, C);
+    engine<D, SCHEME, STATS, true>(sa, W, src, C);
     flush_counters<STATS>(sa, C);
 }
 
