@@ -1,5 +1,5 @@
 """One girg_edges call on a BASELINE config (product generators, kappa from girg_scale_weights),
-for profiling under ncu:  python tools/prof_one.py C4 [merged|event] [reps]"""
+for profiling under ncu:  python tools/prof_one.py C4 [merged|event|refined] [reps]"""
 import os
 import sys
 
@@ -10,7 +10,7 @@ import paper_1905_06706_b200 as girg  # noqa: E402
 from workloads import BY_NAME  # noqa: E402
 
 c = BY_NAME[sys.argv[1] if len(sys.argv) > 1 else "C4"]
-scheme = girg.SCHEME_EVENT if len(sys.argv) > 2 and sys.argv[2] == "event" else girg.SCHEME_MERGED
+scheme = {"event": girg.SCHEME_EVENT, "refined": girg.SCHEME_REFINED}.get(sys.argv[2] if len(sys.argv) > 2 else "", girg.SCHEME_MERGED)
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 stats = not (len(sys.argv) > 4 and sys.argv[4] == "nostats")
 w = girg.weights(c.n, c.beta, c.seed)
