@@ -5,21 +5,24 @@ import csv
 import gzip
 import sys
 
-REGIONS = [  # (file, lo, hi, name): sample.cuh / girg_device.cuh as of the final round-2 code
-    ("sample.cuh", 280, 366, "warp helpers, emit/flush"),
-    ("sample.cuh", 367, 383, "load_rec"),
-    ("sample.cuh", 384, 437, "divmod/chunk_log2/exact"),
-    ("sample.cuh", 438, 589, "setup_common (region, ranges, children)"),
-    ("sample.cuh", 590, 939, "setup_job (classify, prefixes, offsets)"),
-    ("sample.cuh", 940, 1061, "locate"),
-    ("sample.cuh", 1062, 1105, "counters/push_items"),
-    ("sample.cuh", 1106, 1266, "tile/item source"),
-    ("sample.cuh", 1267, 1700, "engine loop"),
-    ("girg_device.cuh", 1, 40, "philox/u53"),
-    ("girg_device.cuh", 41, 119, "morton"),
-    ("girg_device.cuh", 120, 196, "det_log/exp (R26, exact paths)"),
-    ("girg_device.cuh", 197, 226, "dist/prob"),
-    ("girg_device.cuh", 227, 400, "fast paths"),
+REGIONS = [  # (file, lo, hi, name): sample.cuh / girg_device.cuh as of the final round-2 code (with R27)
+    ("sample.cuh", 290, 387, "warp helpers, emit/flush"),
+    ("sample.cuh", 388, 404, "load_rec"),
+    ("sample.cuh", 405, 459, "divmod/chunk_log2/exact/make_task"),
+    ("sample.cuh", 460, 621, "setup_common (region, ranges, children)"),
+    ("sample.cuh", 622, 861, "setup_job (classify, prefixes, offsets)"),
+    ("sample.cuh", 862, 985, "setup_job_ref (R27 refined jobs)"),
+    ("sample.cuh", 986, 1113, "setup_job1 (d = 1)"),
+    ("sample.cuh", 1114, 1227, "locate"),
+    ("sample.cuh", 1228, 1271, "counters/push_items"),
+    ("sample.cuh", 1272, 1434, "tile/item source"),
+    ("sample.cuh", 1435, 1738, "engine loop"),
+    ("sample.cuh", 1739, 1786, "engine_cand (T = 0)"),
+    ("girg_device.cuh", 1, 39, "philox/u53"),
+    ("girg_device.cuh", 40, 113, "morton"),
+    ("girg_device.cuh", 114, 196, "det_log/exp (R26, exact paths)"),
+    ("girg_device.cuh", 197, 220, "dist/prob"),
+    ("girg_device.cuh", 221, 400, "fast paths"),
 ]
 
 

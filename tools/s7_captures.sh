@@ -9,6 +9,7 @@ for spec in merged:k_sample merged:k_big refined:k_big; do
   ncu -i /tmp/ev7_${s}_${k}.ncu-rep --page raw --csv > gpurun_out/ev7_raw_C5_${s}_${k}.csv 2>&1
   ncu -i /tmp/ev7_${s}_${k}.ncu-rep --page source --csv --print-source cuda,sass > /tmp/ev7_src_${s}_${k}.csv 2>&1
   python tools/ncu_regions.py /tmp/ev7_src_${s}_${k}.csv > gpurun_out/ev7_regions_C5_${s}_${k}.txt 2>&1
+  python tools/ncu_lines.py /tmp/ev7_src_${s}_${k}.csv 60 > gpurun_out/ev7_lines_C5_${s}_${k}.txt 2>&1
   tail -3 gpurun_out/ev7_ncu_${s}_${k}.log
 done
 ls -la gpurun_out | grep ev7_
