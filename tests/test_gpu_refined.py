@@ -141,3 +141,22 @@ def test_C5_refined_sampled_shard_parity(ref_x):
         gd = torch.from_numpy(g.astype(np.int64)).cuda()
         pos = torch.searchsorted(k, gd).clamp(max=m - 1)
         assert bool((k[pos] == gd).all())
+
+
+def test_refined_randomised_sweep(ref_x):
+    """Seeded random small cases (n, d, T, beta, degree, threshold): clustered and tiny inputs, low and
+    high temperatures, thresholds that refine some or all levels."""
+    rng = np.random.default_rng(2027)
+    for case in range(24):
+        d = int(rng.integers(2, 4))
+        n = int(rng.choice([3, 17, 130, 1000, 4097, 12_345]))
+        T = float(rng.choice([0.05, 0.3, 0.6, 0.95]))
+        beta = float(rng.choice([2.1, 2.5, 3.5]))
+        x = int(rng.choice([-1, 1, 3, 40]))
+        w, xs = synth_inputs(n, d, beta, 1000 + case)
+        if case % 4 == 0:  # clustered positions: crowded cells next to empty ones
+            xs = (xs * 0.05 + 0.4) % 1.0
+        deg = min(float(rng.choice([2.0, 8.0, 30.0])), max(n - 1.5, 0.5))
+        kappa = O.scale_weights(w, deg, d, T, beta) if n > 2 else 0.5
+        ref_x(x)
+        assert_parity(w, xs, d, T, kappa, 77 + case, scheme=girg.SCHEME_REFINED)
