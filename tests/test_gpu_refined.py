@@ -42,6 +42,8 @@ def ref_x():
                                              (2, 0.3, 3.0, 40_000, 8.0), (3, 0.5, 2.5, 50_000, 10.0),
                                              (3, 0.9, 2.9, 300_000, 20.0)])
 def test_refined_parity(d, T, beta, n, deg, x, ref_x):
+    if n >= 300_000 and x in (2, 8):
+        pytest.skip("the large case runs with the default rule and the every-level hook only (suite time)")
     ref_x(x)
     w, xs = synth_inputs(n, d, beta, 17 * d + n % 13)
     kappa = O.scale_weights(w, deg, d, T, beta)
@@ -109,7 +111,7 @@ def test_C3_full_refined_parity(ref_x):
 def test_C5_refined_sampled_shard_parity(ref_x):
     """BASELINE config 5 (n = 2^24, d = 3) with the default level rule, in the launch configuration
     the bench times with --scheme refined: sampled level-3 shards (a corner block, which owns the
-    coarse events of its ancestors, and two interior ones) equal the oracle's, and each is a subset
+    coarse events of its ancestors, and an interior one) equal the oracle's, and each is a subset
     of the full REFINED edge set.  kappa is the oracle's (tests/golden/oracle_kappa.json)."""
     import json
     import os
@@ -132,7 +134,7 @@ def test_C5_refined_sampled_shard_parity(ref_x):
     assert st["landings"] < sm["landings"] and st["cand1"] == sm["cand1"] and st["edges1"] == sm["edges1"]
     k = girg.edge_keys(full)
     assert bool((k[1:] != k[:-1]).all())
-    for lo, hi in ((0, 1), (200, 201), (363, 364)):
+    for lo, hi in ((0, 1), (363, 364)):
         g, o, stg, so, gp = run_both(w, xs, c.d, c.T, kappa, c.seed, shard=(3, lo, hi), scheme=girg.SCHEME_REFINED)
         assert so["nt1"] + so["nt2acc"] == 0 and so["nt2jump"] == stg["neartie_jump"], (so, stg)
         assert np.array_equal(g, o) and np.array_equal(gp, o)
