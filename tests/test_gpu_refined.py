@@ -104,8 +104,8 @@ def test_C3_full_refined_parity(ref_x):
     kappa = O.scale_weights(w, c.avg_deg, c.d, c.T, c.beta)
     g, st, so = assert_parity(w, xs, c.d, c.T, kappa, c.seed, scheme=girg.SCHEME_REFINED)
     assert abs(2 * len(g) / c.n - c.avg_deg) < 0.01 * c.avg_deg
-    _, sm = O.edges(w, xs, c.d, c.T, kappa, c.seed, with_stats=True, scheme=O.SCHEME_MERGED)
-    assert so["landings"] < sm["landings"]  # refined levels exist at this size
+    _, sm = girg.edges(dev(w), dev(xs), c.T, kappa, c.seed, stats=True, scheme=girg.SCHEME_MERGED)
+    assert st["landings"] < sm["landings"]  # refined levels exist at this size
 
 
 def test_C5_refined_sampled_shard_parity(ref_x):
